@@ -185,6 +185,10 @@ void* gen_rrg(int d, int64_t n, double gamma, int n_boxes, double side_lo,
         std::vector<int64_t> cur(cstart.begin(), cstart.end() - 1);
         for (int64_t i = 0; i < n; ++i) cpts[cur[cell_of[i]]++] = (int32_t)i;  // ascending id per cell
     }
+    // coordinates in cell order, so that scanning a cell reads contiguous memory
+    std::vector<double> cpos((size_t)n * d);
+    for (int64_t t = 0; t < n; ++t)
+        std::memcpy(&cpos[(size_t)t * d], &G->pts[(size_t)cpts[t] * d], sizeof(double) * d);
 
     std::vector<std::vector<std::pair<int32_t, double>>> nb(n);
     std::vector<int64_t> cand_count(n, 0);
@@ -193,15 +197,23 @@ void* gen_rrg(int d, int64_t n, double gamma, int n_boxes, double side_lo,
         const double R = radius(gamma, i + 1, d);
         auto& out = nb[i];
         int64_t cand = 0;
-        auto consider = [&](int32_t j) {
+        const double R2 = R * R;
+        auto consider_at = [&](int32_t j, const double* q) {
             ++cand;
-            const double* q = &G->pts[(size_t)j * d];
-            double dd = dist(p, q, d);
+            // squared distance with early exit; same summation order as dist()
+            double s2 = 0.0;
+            for (int k = 0; k < d; ++k) {
+                double t = p[k] - q[k];
+                s2 += t * t;
+                if (s2 > R2 * (1.0 + 1e-12)) return;
+            }
+            double dd = std::sqrt(s2);
             if (dd > R) return;
             for (int bI = 0; bI < n_boxes; ++bI)
                 if (seg_hits_box(q, p, &G->boxes[(size_t)bI * 2 * d], d)) return;
             out.push_back({j, dd});
         };
+        auto consider = [&](int32_t j) { consider_at(j, &G->pts[(size_t)j * d]); };
         int kr = (int)std::ceil(R / side);
         double cells_scanned = std::pow(2.0 * kr + 1.0, d);
         if (kr >= m || cells_scanned * (1.0 + (double)n / ncell) > (double)i) {
@@ -220,7 +232,7 @@ void* gen_rrg(int d, int64_t n, double gamma, int n_boxes, double side_lo,
                 for (int64_t t = cstart[c]; t < cstart[c + 1]; ++t) {
                     int32_t j = cpts[t];
                     if (j >= i) break;  // ascending ids in a cell
-                    consider(j);
+                    consider_at(j, &cpos[(size_t)t * d]);
                 }
                 int k = d - 1;
                 while (k >= 0 && cc[k] == hi[k]) { cc[k] = lo[k]; --k; }

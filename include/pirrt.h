@@ -1,0 +1,173 @@
+/*
+ * pirrt.h -- C ABI of the B200-native PI-RRT# exploitation library
+ * (libpirrt.so, paper_2003_04920_b200/lib/).
+ *
+ * Method: the exploitation phase of PI-RRT# / BE-RRT#, arXiv 2003.04920
+ * ("PAPER.md" below): policy iteration on the random geometric graph
+ * G = (V, E) with edge costs c : E -> R+, a root x_init, a goal x_goal and an
+ * admissible heuristic h : V -> R+ (problem statement PAPER.md:168-178),
+ * iterated to a fixed point after each single or batched graph extension
+ * (Alg. 2; Alg. 3).  Ambiguities of the
+ * listing are resolved by the readings R1-R14 of DESIGN.md section 3.
+ *
+ * Conventions for every call:
+ *   - Vertex ids are dense int32 0..n-1; -1 means "no vertex".  Vertex 0 is
+ *     x_init (g = 0) and vertex 1 is x_goal (g = +inf); both exist after
+ *     pirrt_create (Alg. 1 line 1).
+ *   - All floating point is IEEE binary64.  Costs and h must be finite and
+ *     >= 0; -0.0 is stored as +0.0 (R12).
+ *   - Ownership: the caller owns every input and output array; the library
+ *     copies inputs before returning and owns all device memory.  Unless the
+ *     call's flags contain PIRRT_F_DEVICE_PTRS, pointers are host pointers
+ *     (pinned host memory makes the H2D copies asynchronous DMA).  Every call
+ *     is synchronous with respect to the context's stream: when it returns,
+ *     results are visible to the caller.
+ *   - Errors: every call returns PIRRT_OK (0) or a negative PIRRT_E_* code and
+ *     sets a thread-local message readable with pirrt_last_error().  On error
+ *     the context state (graph, policy, costs, promising set) is unchanged,
+ *     except after PIRRT_E_CUDA, which leaves the context unusable.
+ *   - A context is single-threaded; separate contexts are independent.
+ */
+#ifndef PIRRT_H
+#define PIRRT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pirrt_ctx pirrt_ctx;  /* opaque; owned by the library */
+typedef int32_t pirrt_vid;           /* vertex id, dense; -1 = none  */
+
+enum {
+    PIRRT_OK = 0,
+    PIRRT_E_INVAL = -1,   /* bad argument: NaN/inf/negative cost or h, self-loop, NULL */
+    PIRRT_E_RANGE = -2,   /* vertex id out of range, or output capacity too small   */
+    PIRRT_E_NOMEM = -3,   /* device or pinned host allocation failed                 */
+    PIRRT_E_CUDA = -4,    /* CUDA runtime error (context unusable afterwards)        */
+    PIRRT_E_NCCL = -5,    /* multi-GPU communication error                           */
+    PIRRT_E_NOCONV = -6,  /* exploit exceeded max_iterations (R11)       */
+    PIRRT_E_STATE = -7,   /* call out of order / unsupported configuration           */
+    PIRRT_E_CORRUPT = -8  /* parent cycle or missing policy edge detected            */
+};
+
+enum {
+    /* config flags */
+    PIRRT_F_PRUNE_OFF = 1u,        /* I = V \ {root}, thr = +inf: classical PI (test/cold mode) */
+    PIRRT_F_VALIDATE = 2u,         /* extra checks: g_new consistency                           */
+    /* append flags */
+    PIRRT_F_EDGES_UNDIRECTED = 4u, /* each (src,dst,cost) is stored in both directions         */
+    PIRRT_F_DEVICE_PTRS = 8u       /* input arrays are device pointers (e.g. torch CUDA tensors)*/
+};
+
+typedef struct {
+    int64_t vertex_capacity;  /* initial reservation (hint; the store grows past it)        */
+    int64_t edge_capacity;    /* initial directed-edge reservation (hint)                    */
+    double h_root;            /* h(x_init); default 0                                       */
+    double h_goal;            /* h(x_goal); default 0                                       */
+    double epsilon;           /* stop when Delta g <= epsilon (R5); default 0               */
+    int32_t max_iterations;   /* Improve cap per exploit; 0 -> 10 |V| (R11)                  */
+    uint32_t flags;           /* PIRRT_F_PRUNE_OFF | PIRRT_F_VALIDATE                        */
+    int32_t device;           /* CUDA device ordinal                                        */
+    void* stream;             /* cudaStream_t to run on (e.g. a torch stream); NULL: own one */
+    int32_t grid_blocks;      /* persistent-kernel grid; 0 = auto (SMs x occupancy)          */
+    int32_t nranks;           /* multi-GPU SPMD: ranks (1 = single GPU)                      */
+    int32_t rank;             /* this process's rank                                        */
+    const void* nccl_unique_id; /* ncclUniqueId (128 B) shared by all ranks when nranks > 1  */
+} pirrt_config;
+
+typedef struct {
+    int32_t iterations;      /* Improve calls (Alg. 2)                          */
+    int32_t evaluations;     /* Evaluate calls                                           */
+    double last_delta_g;     /* Delta g of the final Improve                             */
+    int64_t relaxations;     /* sum over Improves of sum_{v in I} indeg(v)               */
+    int64_t eval_visits;     /* children visited, summed over Evaluates                  */
+    int32_t max_level;       /* deepest Evaluate BFS level reached (root = 0)            */
+    int32_t promising;       /* |B| on return                                            */
+    int32_t stalled;         /* 1 if the R13 stall guard ended the loop                  */
+    int32_t grid_blocks;     /* persistent grid used                                     */
+    float device_ms;         /* exploit kernel time, CUDA events on the context stream   */
+    float improve_ms;        /* time inside Improve phases (device %globaltimer)         */
+    float evaluate_ms;       /* time inside Evaluate phases incl. children index         */
+    float compact_ms;        /* time inside promising-set compaction phases              */
+    int64_t improve_set;     /* sum over Improves of |I| (vertices examined)             */
+    int64_t children_index;  /* vertices scanned by children-index rebuilds              */
+} pirrt_exploit_stats;
+
+/* Fill *cfg with the defaults listed above. */
+void pirrt_config_init(pirrt_config* cfg);
+
+/* Create a context on cfg->device: V = {x_init (g=0, h=h_root), x_goal
+ * (g=+inf, h=h_goal)}, E = {}, B = {} (Alg. 1 line 1). */
+int pirrt_create(const pirrt_config* cfg, pirrt_ctx** out);
+int pirrt_destroy(pirrt_ctx* ctx);
+
+/* Append one extension batch (Alg. 3 lines 6-8; data flow
+ * each edge is sent to the device exactly once).
+ *   n_new       new vertices; they get ids [n, n + n_new) in caller order.
+ *   h_new       [n_new] heuristic of the new vertices.
+ *   parent_new, g_new  [n_new] the new vertices' policy and cost-to-come, or
+ *               both NULL: the library then performs Extend's local
+ *               relaxation (reading R14): in increasing id
+ *               order g(v) = min over edges (u -> v), u < v, of g(u) + c(u,v),
+ *               lowest u on ties; +inf and parent -1 if there is none.  When
+ *               given, the edge (parent_new[i] -> new vertex i) must be in the
+ *               batch (its cost becomes the policy-edge cost).
+ *   n_edges, src, dst, cost  [n_edges] COO edges; (src, dst, c) means "dst
+ *               may take src as parent at cost c" = c(n, v) with n = src,
+ *               v = dst.  Endpoints may be old or new vertices.
+ *               With PIRRT_F_EDGES_UNDIRECTED each triple is stored both ways.
+ *   n_new_promising (out, nullable)  number of new vertices with
+ *               g + h < g(x_goal), i.e. |B'| - |B| for the
+ *               Alg. 3 replan guard (reading R10).
+ * Errors: E_RANGE endpoint >= n + n_new or < 0; E_INVAL non-finite/negative
+ * cost or h, self-loop, only one of parent_new/g_new given, missing parent
+ * edge.  Duplicate (src,dst) pairs are the caller's responsibility (SPEC
+ * S:128); Improve takes the cheapest of duplicates. */
+int pirrt_graph_append_batch(pirrt_ctx* ctx, int32_t n_new, const double* h_new,
+                             const pirrt_vid* parent_new, const double* g_new,
+                             int64_t n_edges, const pirrt_vid* src, const pirrt_vid* dst,
+                             const double* cost, uint32_t flags, int32_t* n_new_promising);
+
+/* Replan (Alg. 2) to a fixed point, entirely on the device:
+ * loop { Improve over I = B u {x_goal} \ {x_init};
+ *        if Delta g <= epsilon break; Evaluate }.
+ * Improve: each v in I takes the lowest-id argmin over its in-edges of
+ * g(u) + c(u,v) if strictly below g(v); g is not written (Jacobi).
+ * Evaluate: thr = g(x_goal) snapshot; truncated BFS of the policy tree from
+ * x_init, g(n) = g(parent) + c(parent, n), expand and mark promising iff
+ * g(n) + h(n) < thr.  stats (nullable) receives counters and timings.
+ * Errors: E_NOCONV after max_iterations Improves (state as left). */
+int pirrt_exploit(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
+
+/* Read-out (host outputs, cap >= pirrt_num_vertices or E_RANGE, nothing written). */
+int pirrt_get_policy(const pirrt_ctx* ctx, pirrt_vid* parent_out, int64_t cap);
+int pirrt_get_costs(const pirrt_ctx* ctx, double* g_out, int64_t cap);
+int pirrt_get_promising(const pirrt_ctx* ctx, uint8_t* b_out, int64_t cap);
+int pirrt_get_parent_costs(const pirrt_ctx* ctx, double* pc_out, int64_t cap);
+
+/* Policy-tree extraction (Alg. 1 lines 8-12): the goal
+ * branch root..x_goal into path_out[0..len).  Unreached goal: *len_out = 0,
+ * *cost_out = +inf.  E_RANGE if cap < path length (nothing written);
+ * E_CORRUPT if the branch does not reach the root. */
+int pirrt_best_path(const pirrt_ctx* ctx, pirrt_vid* path_out, int64_t cap,
+                    int64_t* len_out, double* cost_out);
+
+/* Restore a policy snapshot (host arrays of length n): parent, g, and b
+ * (nullable -> B = {}).  The policy-edge cost of v is re-read from the stored
+ * edge (parent(v) -> v) (R9); E_INVAL if it is missing or the root is not
+ * (parent -1, g 0). */
+int pirrt_set_policy(pirrt_ctx* ctx, const pirrt_vid* parent, const double* g,
+                     const uint8_t* b);
+
+int64_t pirrt_num_vertices(const pirrt_ctx* ctx);
+int64_t pirrt_num_edges(const pirrt_ctx* ctx);   /* directed edges stored */
+/* Number of CUDA kernels this context has launched so far (diagnostics). */
+int64_t pirrt_kernel_launches(const pirrt_ctx* ctx);
+const char* pirrt_last_error(void);              /* thread-local; valid until the next call */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIRRT_H */

@@ -1,0 +1,547 @@
+// abi.cu -- the C ABI of include/pirrt.h: context, device memory, staging,
+// and the host side of every call.  The hot path (exploit) is one
+// cooperative kernel launch; append is a short chain of kernels with one
+// host synchronisation at the end (for n_new_promising and the validation
+// verdict).  No CPU fallback exists: every result is computed on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace pirrt;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                   \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess)                                                     \
+            return fail(PIRRT_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// device allocation that grows geometrically; keep_bytes are preserved
+template <class T>
+int grow(T*& p, int64_t& cap, int64_t need, int64_t keep, cudaStream_t s) {
+    if (need <= cap) return 0;
+    int64_t nc = std::max<int64_t>(need, cap + cap / 2);
+    nc = std::max<int64_t>(nc, 64);
+    T* q = nullptr;
+    if (cudaMalloc(&q, (size_t)nc * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PIRRT_E_NOMEM, "cudaMalloc failed");
+    }
+    if (p) {
+        if (keep > 0) CU(cudaMemcpyAsync(q, p, (size_t)keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        CU(cudaStreamSynchronize(s));
+        CU(cudaFree(p));
+    }
+    p = q;
+    cap = nc;
+    return 0;
+}
+
+std::string err_bits(int e) {
+    std::string m;
+    if (e & kErrRange) m += " id out of range;";
+    if (e & kErrSelfLoop) m += " self-loop;";
+    if (e & kErrCost) m += " cost not finite and >= 0;";
+    if (e & kErrH) m += " h not finite and >= 0;";
+    if (e & kErrGNew) m += " bad g (given policy);";
+    if (e & kErrPcMissing) m += " policy edge (parent -> v) not stored;";
+    if (e & kErrRoot) m += " root must have parent -1 and g 0;";
+    return m;
+}
+
+}  // namespace
+
+struct pirrt_ctx {
+    pirrt_config cfg;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 0;
+    int grid_blocks = 0;
+    int n = 0;
+    int64_t vcap = 0;
+    // vertex SoA
+    double* g = nullptr; int64_t g_cap = 0;
+    double* h = nullptr; int64_t h_cap = 0;
+    double* pc = nullptr; int64_t pc_cap = 0;
+    int* parent = nullptr; int64_t parent_cap = 0;
+    unsigned char* b = nullptr; int64_t b_cap = 0;
+    // base CSR
+    long long* boff = nullptr; int64_t boff_cap = 0;
+    int* bidx = nullptr; int64_t bidx_cap = 0;
+    double* bcost = nullptr; int64_t bcost_cap = 0;
+    int64_t base_edges = 0;
+    // delta CSR, double-buffered (cur = committed)
+    long long* doff[2] = {nullptr, nullptr}; int64_t doff_cap[2] = {0, 0};
+    int* didx[2] = {nullptr, nullptr}; int64_t didx_cap[2] = {0, 0};
+    double* dcost[2] = {nullptr, nullptr}; int64_t dcost_cap[2] = {0, 0};
+    int cur = 0;
+    int64_t delta_edges = 0;
+    // scratch
+    long long* cnt = nullptr; int64_t cnt_cap = 0;
+    long long* scan_tmp = nullptr; int64_t scan_cap = 0;
+    // exploit workspace
+    int* Ilist = nullptr; int64_t Ilist_cap = 0;
+    int* kcnt = nullptr; int64_t kcnt_cap = 0;
+    int* krank = nullptr; int64_t krank_cap = 0;
+    int* koff = nullptr; int64_t koff_cap = 0;
+    int* kids = nullptr; int64_t kids_cap = 0;
+    int* front0 = nullptr; int64_t front0_cap = 0;
+    int* front1 = nullptr; int64_t front1_cap = 0;
+    long long* bsum = nullptr; int64_t bsum_cap = 0;
+    DevCtl* ctl = nullptr;
+    DevCtl* ctl_host = nullptr;   // pinned mirror
+    // staging for host inputs
+    int* s_src = nullptr; int64_t s_src_cap = 0;
+    int* s_dst = nullptr; int64_t s_dst_cap = 0;
+    double* s_cost = nullptr; int64_t s_cost_cap = 0;
+    double* s_h = nullptr; int64_t s_h_cap = 0;
+    int* s_parent = nullptr; int64_t s_parent_cap = 0;
+    double* s_g = nullptr; int64_t s_g_cap = 0;
+    double* s_pc = nullptr; int64_t s_pc_cap = 0;
+    unsigned char* s_b = nullptr; int64_t s_b_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool broken = false;
+    int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
+};
+
+namespace {
+
+int set_device(const pirrt_ctx* c) {
+    CU(cudaSetDevice(c->cfg.device));
+    if (c->broken) return fail(PIRRT_E_STATE, "context unusable after an earlier CUDA error");
+    return 0;
+}
+
+// make every per-vertex array hold at least `need` vertices (+1 for offsets)
+int ensure_vertices(pirrt_ctx* c, int64_t need) {
+    if (need <= c->vcap) return 0;
+    int64_t cap = std::max<int64_t>(need, c->vcap + c->vcap / 2);
+    cap = std::max<int64_t>(cap, 1024);
+    const int64_t n = c->n;
+    cudaStream_t s = c->stream;
+    int rc;
+    if ((rc = grow(c->g, c->g_cap, cap, n, s))) return rc;
+    if ((rc = grow(c->h, c->h_cap, cap, n, s))) return rc;
+    if ((rc = grow(c->pc, c->pc_cap, cap, n, s))) return rc;
+    if ((rc = grow(c->parent, c->parent_cap, cap, n, s))) return rc;
+    if ((rc = grow(c->b, c->b_cap, cap, n, s))) return rc;
+    if ((rc = grow(c->boff, c->boff_cap, cap + 1, n + 1, s))) return rc;
+    if ((rc = grow(c->doff[c->cur], c->doff_cap[c->cur], cap + 1, n + 1, s))) return rc;
+    if ((rc = grow(c->doff[1 - c->cur], c->doff_cap[1 - c->cur], cap + 1, 0, s))) return rc;
+    if ((rc = grow(c->cnt, c->cnt_cap, cap + 1, 0, s))) return rc;
+    if ((rc = grow(c->scan_tmp, c->scan_cap, (int64_t)scan_tmp_elems(cap + 1), 0, s))) return rc;
+    if ((rc = grow(c->Ilist, c->Ilist_cap, cap, 0, s))) return rc;
+    if ((rc = grow(c->kcnt, c->kcnt_cap, cap + 1, 0, s))) return rc;
+    if ((rc = grow(c->krank, c->krank_cap, cap, 0, s))) return rc;
+    if ((rc = grow(c->koff, c->koff_cap, cap + 1, 0, s))) return rc;
+    if ((rc = grow(c->kids, c->kids_cap, cap, 0, s))) return rc;
+    if ((rc = grow(c->front0, c->front0_cap, cap, 0, s))) return rc;
+    if ((rc = grow(c->front1, c->front1_cap, cap, 0, s))) return rc;
+    c->vcap = cap;
+    return 0;
+}
+
+void free_all(pirrt_ctx* c) {
+    void* ptrs[] = {c->g, c->h, c->pc, c->parent, c->b, c->boff, c->bidx, c->bcost,
+                    c->doff[0], c->doff[1], c->didx[0], c->didx[1], c->dcost[0], c->dcost[1],
+                    c->cnt, c->scan_tmp, c->Ilist, c->kcnt, c->krank, c->koff, c->kids,
+                    c->front0, c->front1, c->bsum, c->ctl, c->s_src, c->s_dst, c->s_cost,
+                    c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->ctl_host) cudaFreeHost(c->ctl_host);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+template <class T>
+int stage(pirrt_ctx* c, const T* src, int64_t count, bool device, T*& buf, int64_t& cap,
+          const T** out) {
+    if (count == 0 || src == nullptr) { *out = src; return 0; }
+    if (device) { *out = src; return 0; }
+    int rc;
+    if ((rc = grow(buf, cap, count, 0, c->stream))) return rc;
+    CU(cudaMemcpyAsync(buf, src, (size_t)count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    *out = buf;
+    return 0;
+}
+
+int read_ctl(pirrt_ctx* c) {
+    CU(cudaMemcpyAsync(c->ctl_host, c->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
+    // fold the delta into the base when it outgrows sqrt(8 m |base|) (and 32k
+    // edges): per-append merge cost O(delta) balances amortised O(|E|)
+    // compaction cost
+    double thr = std::sqrt(8.0 * (double)std::max<int64_t>(m_dir, 1) * (double)c->base_edges);
+    thr = std::max(thr, 32768.0);
+    if ((double)c->delta_edges <= thr) return 0;
+    const int64_t E = c->base_edges + c->delta_edges;
+    long long* nboff = nullptr; int64_t nboff_cap = 0;
+    int* nbidx = nullptr; int64_t nbidx_cap = 0;
+    double* nbcost = nullptr; int64_t nbcost_cap = 0;
+    int rc;
+    if ((rc = grow(nboff, nboff_cap, c->vcap + 1, 0, c->stream))) return rc;
+    if ((rc = grow(nbidx, nbidx_cap, E + E / 4, 0, c->stream))) return rc;
+    if ((rc = grow(nbcost, nbcost_cap, E + E / 4, 0, c->stream))) return rc;
+    CompactArgs a;
+    a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
+    a.doff = c->doff[c->cur]; a.didx = c->didx[c->cur]; a.dcost = c->dcost[c->cur];
+    a.boff_new = nboff; a.bidx_new = nbidx; a.bcost_new = nbcost;
+    a.cnt = c->cnt; a.scan_tmp = c->scan_tmp; a.n = c->n;
+    const long long l0 = g_kernel_launches;
+    CU(launch_compact(a, c->stream));
+    c->launches += g_kernel_launches - l0;
+    CU(cudaMemsetAsync(c->doff[c->cur], 0, (size_t)(c->n + 1) * sizeof(long long), c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (c->boff) cudaFree(c->boff);
+    if (c->bidx) cudaFree(c->bidx);
+    if (c->bcost) cudaFree(c->bcost);
+    c->boff = nboff; c->boff_cap = nboff_cap;
+    c->bidx = nbidx; c->bidx_cap = nbidx_cap;
+    c->bcost = nbcost; c->bcost_cap = nbcost_cap;
+    c->base_edges = E;
+    c->delta_edges = 0;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+void pirrt_config_init(pirrt_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->nranks = 1;
+}
+
+const char* pirrt_last_error(void) { return g_err.c_str(); }
+
+int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
+    if (!cfg_in || !out) return fail(PIRRT_E_INVAL, "create: NULL argument");
+    const pirrt_config& cfg = *cfg_in;
+    if (!(cfg.h_root >= 0.0) || !(cfg.h_goal >= 0.0) || std::isinf(cfg.h_root) ||
+        std::isinf(cfg.h_goal) || !(cfg.epsilon >= 0.0) || cfg.max_iterations < 0)
+        return fail(PIRRT_E_INVAL, "create: invalid h_root/h_goal/epsilon/max_iterations");
+    if (cfg.nranks > 1)
+        return fail(PIRRT_E_STATE, "create: multi-GPU mode (nranks > 1) is not built in this version");
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (cfg.device < 0 || cfg.device >= ndev) return fail(PIRRT_E_INVAL, "create: bad device");
+    CU(cudaSetDevice(cfg.device));
+    pirrt_ctx* c = new pirrt_ctx();
+    c->cfg = cfg;
+    auto bail = [&](int rc) { free_all(c); delete c; return rc; };
+    if (cfg.stream) {
+        c->stream = (cudaStream_t)cfg.stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(PIRRT_E_CUDA, "create: stream"));
+        c->own_stream = true;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cfg.device) != cudaSuccess)
+        return bail(fail(PIRRT_E_CUDA, "create: device properties"));
+    c->num_sms = prop.multiProcessorCount;
+    if (!prop.cooperativeLaunch) return bail(fail(PIRRT_E_STATE, "create: no cooperative launch"));
+    int per_sm = exploit_blocks_per_sm();
+    if (per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: exploit kernel does not fit an SM"));
+    c->grid_blocks = cfg.grid_blocks > 0 ? std::min(cfg.grid_blocks, per_sm * c->num_sms)
+                                         : per_sm * c->num_sms;
+    int rc;
+    int64_t vcap0 = std::max<int64_t>(cfg.vertex_capacity, 1024);
+    if ((rc = ensure_vertices(c, vcap0))) return bail(rc);
+    int64_t ecap0 = std::max<int64_t>(cfg.edge_capacity, 4096);
+    for (int k = 0; k < 2; ++k) {
+        if ((rc = grow(c->didx[k], c->didx_cap[k], ecap0, 0, c->stream))) return bail(rc);
+        if ((rc = grow(c->dcost[k], c->dcost_cap[k], ecap0, 0, c->stream))) return bail(rc);
+    }
+    if ((rc = grow(c->bidx, c->bidx_cap, 64, 0, c->stream))) return bail(rc);
+    if ((rc = grow(c->bcost, c->bcost_cap, 64, 0, c->stream))) return bail(rc);
+    if ((rc = grow(c->bsum, c->bsum_cap, c->grid_blocks + 1, 0, c->stream))) return bail(rc);
+    if (cudaMalloc(&c->ctl, sizeof(DevCtl)) != cudaSuccess) return bail(fail(PIRRT_E_NOMEM, "ctl"));
+    if (cudaMallocHost(&c->ctl_host, sizeof(DevCtl)) != cudaSuccess)
+        return bail(fail(PIRRT_E_NOMEM, "ctl host"));
+    if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
+        return bail(fail(PIRRT_E_CUDA, "events"));
+    // V = {x_init, x_goal}, E = {}, B = {}
+    const double g0[2] = {0.0, INFINITY};
+    const double h0[2] = {cfg.h_root + 0.0, cfg.h_goal + 0.0};
+    const int p0[2] = {-1, -1};
+    cudaStream_t s = c->stream;
+    if (cudaMemcpyAsync(c->g, g0, sizeof g0, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(c->h, h0, sizeof h0, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(c->parent, p0, sizeof p0, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemsetAsync(c->pc, 0, 2 * sizeof(double), s) != cudaSuccess ||
+        cudaMemsetAsync(c->b, 0, 2, s) != cudaSuccess ||
+        cudaMemsetAsync(c->boff, 0, 3 * sizeof(long long), s) != cudaSuccess ||
+        cudaMemsetAsync(c->doff[0], 0, 3 * sizeof(long long), s) != cudaSuccess ||
+        cudaMemsetAsync(c->ctl, 0, sizeof(DevCtl), s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(fail(PIRRT_E_CUDA, "create: init copies"));
+    c->n = 2;
+    *out = c;
+    return PIRRT_OK;
+}
+
+int pirrt_destroy(pirrt_ctx* c) {
+    if (!c) return PIRRT_OK;
+    cudaSetDevice(c->cfg.device);
+    cudaStreamSynchronize(c->stream);
+    free_all(c);
+    delete c;
+    return PIRRT_OK;
+}
+
+int64_t pirrt_num_vertices(const pirrt_ctx* c) { return c ? c->n : 0; }
+int64_t pirrt_num_edges(const pirrt_ctx* c) { return c ? c->base_edges + c->delta_edges : 0; }
+int64_t pirrt_kernel_launches(const pirrt_ctx* c) { return c ? c->launches : 0; }
+
+int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
+                             const pirrt_vid* parent_new, const double* g_new, int64_t n_edges,
+                             const pirrt_vid* src, const pirrt_vid* dst, const double* cost,
+                             uint32_t flags, int32_t* n_new_promising) {
+    if (!c) return fail(PIRRT_E_INVAL, "append: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if (n_new < 0 || n_edges < 0) return fail(PIRRT_E_INVAL, "append: negative size");
+    if ((parent_new == nullptr) != (g_new == nullptr))
+        return fail(PIRRT_E_INVAL, "append: parent_new and g_new must both be given or both NULL");
+    if (n_new > 0 && !h_new) return fail(PIRRT_E_INVAL, "append: h_new is NULL");
+    if (n_edges > 0 && (!src || !dst || !cost)) return fail(PIRRT_E_INVAL, "append: NULL edge array");
+    if ((int64_t)c->n + n_new > INT32_MAX - 1) return fail(PIRRT_E_RANGE, "append: too many vertices");
+    const bool dev = (flags & PIRRT_F_DEVICE_PTRS) != 0;
+    const bool undirected = (flags & PIRRT_F_EDGES_UNDIRECTED) != 0;
+    const int64_t m_dir = undirected ? 2 * n_edges : n_edges;
+    const int n_old = c->n, n_all = c->n + n_new;
+    cudaStream_t s = c->stream;
+    // capacity (growth does not change state)
+    if ((rc = ensure_vertices(c, n_all))) return rc;
+    const int nb = 1 - c->cur;
+    const int64_t dneed = c->delta_edges + m_dir;
+    if ((rc = grow(c->didx[nb], c->didx_cap[nb], dneed, 0, s))) return rc;
+    if ((rc = grow(c->dcost[nb], c->dcost_cap[nb], dneed, 0, s))) return rc;
+    // inputs
+    const double *d_h = nullptr, *d_g = nullptr, *d_cost = nullptr;
+    const int *d_parent = nullptr, *d_src = nullptr, *d_dst = nullptr;
+    if ((rc = stage(c, h_new, n_new, dev, c->s_h, c->s_h_cap, &d_h))) return rc;
+    if ((rc = stage(c, parent_new, n_new, dev, c->s_parent, c->s_parent_cap, &d_parent))) return rc;
+    if ((rc = stage(c, g_new, n_new, dev, c->s_g, c->s_g_cap, &d_g))) return rc;
+    if ((rc = stage(c, src, n_edges, dev, c->s_src, c->s_src_cap, &d_src))) return rc;
+    if ((rc = stage(c, dst, n_edges, dev, c->s_dst, c->s_dst_cap, &d_dst))) return rc;
+    if ((rc = stage(c, cost, n_edges, dev, c->s_cost, c->s_cost_cap, &d_cost))) return rc;
+    CU(cudaMemsetAsync(&c->ctl->err, 0, 4 * sizeof(int), s));   // err, nprom, sweeps
+    CU(cudaMemsetAsync(&c->ctl->sweep_changed[0], 0, 2 * sizeof(int), s));
+    AppendArgs a;
+    a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
+    a.doff_old = c->doff[c->cur]; a.didx_old = c->didx[c->cur]; a.dcost_old = c->dcost[c->cur];
+    a.doff_new = c->doff[nb]; a.didx_new = c->didx[nb]; a.dcost_new = c->dcost[nb];
+    a.boff_w = c->boff;
+    a.cnt = c->cnt; a.scan_tmp = c->scan_tmp;
+    a.h_in = d_h; a.parent_in = parent_new ? d_parent : nullptr; a.g_in = g_new ? d_g : nullptr;
+    a.src = d_src; a.dst = d_dst; a.cost = d_cost; a.m = n_edges;
+    a.undirected = undirected ? 1 : 0;
+    a.validate = ((flags | c->cfg.flags) & PIRRT_F_VALIDATE) ? 1 : 0;
+    a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
+    a.n_old = n_old; a.n_new = n_new; a.base_edges = c->base_edges;
+    a.ctl = c->ctl;
+    a.grid_blocks = c->num_sms;
+    const long long l0 = g_kernel_launches;
+    cudaError_t e = launch_append(a, s);
+    c->launches += g_kernel_launches - l0;
+    if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("append: ") + cudaGetErrorString(e)); }
+    if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+    const int err = c->ctl_host->err;
+    if (err) {
+        int code = (err & (kErrRange)) ? PIRRT_E_RANGE : PIRRT_E_INVAL;
+        return fail(code, "append rejected:" + err_bits(err));
+    }
+    // commit
+    c->cur = nb;
+    c->n = n_all;
+    c->delta_edges += m_dir;
+    if (n_new_promising) *n_new_promising = c->ctl_host->nprom;
+    if ((rc = compact_if_needed(c, m_dir))) { c->broken = true; return rc; }
+    return PIRRT_OK;
+}
+
+int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
+    if (!c) return fail(PIRRT_E_INVAL, "exploit: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    cudaStream_t s = c->stream;
+    CU(cudaMemsetAsync(c->ctl, 0, offsetof(DevCtl, err), s));
+    ExploitArgs a;
+    a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
+    a.doff = c->doff[c->cur]; a.didx = c->didx[c->cur]; a.dcost = c->dcost[c->cur];
+    a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
+    a.Ilist = c->Ilist; a.kcnt = c->kcnt; a.krank = c->krank; a.koff = c->koff; a.kids = c->kids;
+    a.front0 = c->front0; a.front1 = c->front1; a.bsum = c->bsum;
+    a.ctl = c->ctl;
+    a.n = c->n;
+    a.max_it = c->cfg.max_iterations;
+    a.eps = c->cfg.epsilon;
+    a.prune_off = (c->cfg.flags & PIRRT_F_PRUNE_OFF) ? 1 : 0;
+    CU(cudaEventRecord(c->ev0, s));
+    const long long l0 = g_kernel_launches;
+    cudaError_t e = launch_exploit(a, c->grid_blocks, s);
+    c->launches += g_kernel_launches - l0;
+    if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
+    CU(cudaEventRecord(c->ev1, s));
+    if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+    const DevCtl& h = *c->ctl_host;
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->iterations = h.iterations;
+        st->evaluations = h.evaluations;
+        st->last_delta_g = h.last_dg;
+        st->relaxations = h.relaxations;
+        st->eval_visits = h.eval_visits;
+        st->max_level = h.max_level;
+        st->promising = h.promising;
+        st->stalled = h.stalled;
+        st->grid_blocks = c->grid_blocks;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+        st->device_ms = ms;
+        st->improve_ms = (float)(h.t_improve * 1e-6);
+        st->evaluate_ms = (float)(h.t_evaluate * 1e-6);
+        st->compact_ms = (float)(h.t_compact * 1e-6);
+        st->improve_set = h.improve_set;
+        st->children_index = h.children_index;
+    }
+    if (h.status == PIRRT_E_NOCONV) return fail(PIRRT_E_NOCONV, "exploit: iteration cap exceeded");
+    return PIRRT_OK;
+}
+
+static int get_array(const pirrt_ctx* c, void* out, const void* dsrc, size_t elem, int64_t cap,
+                     const char* what) {
+    if (!c || !out) return fail(PIRRT_E_INVAL, std::string(what) + ": NULL argument");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if (cap < c->n) return fail(PIRRT_E_RANGE, std::string(what) + ": capacity too small");
+    CU(cudaMemcpyAsync(out, dsrc, (size_t)c->n * elem, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return PIRRT_OK;
+}
+
+int pirrt_get_policy(const pirrt_ctx* c, pirrt_vid* out, int64_t cap) {
+    return get_array(c, out, c ? c->parent : nullptr, sizeof(int), cap, "get_policy");
+}
+int pirrt_get_costs(const pirrt_ctx* c, double* out, int64_t cap) {
+    return get_array(c, out, c ? c->g : nullptr, sizeof(double), cap, "get_costs");
+}
+int pirrt_get_promising(const pirrt_ctx* c, uint8_t* out, int64_t cap) {
+    return get_array(c, out, c ? c->b : nullptr, 1, cap, "get_promising");
+}
+int pirrt_get_parent_costs(const pirrt_ctx* c, double* out, int64_t cap) {
+    return get_array(c, out, c ? c->pc : nullptr, sizeof(double), cap, "get_parent_costs");
+}
+
+int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64_t* len_out,
+                    double* cost_out) {
+    pirrt_ctx* c = const_cast<pirrt_ctx*>(cc);
+    if (!c) return fail(PIRRT_E_INVAL, "best_path: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    cudaStream_t s = c->stream;
+    // path_rev lives in front1 (workspace, n entries), its length in kcnt[n]
+    const long long l0 = g_kernel_launches;
+    CU(launch_best_path(c->parent, c->n, c->front1, c->kcnt + c->n, s));
+    c->launches += g_kernel_launches - l0;
+    int len = 0;
+    double gg = 0.0;
+    CU(cudaMemcpyAsync(&len, c->kcnt + c->n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&gg, c->g + kGoal, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (std::isinf(gg)) {
+        if (len_out) *len_out = 0;
+        if (cost_out) *cost_out = INFINITY;
+        return PIRRT_OK;
+    }
+    if (len < 0) return fail(PIRRT_E_CORRUPT, "best_path: parent cycle");
+    std::vector<int> rev(len);
+    CU(cudaMemcpyAsync(rev.data(), c->front1, (size_t)len * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (len == 0 || rev.back() != kRoot)
+        return fail(PIRRT_E_CORRUPT, "best_path: goal branch does not reach the root");
+    if (cap < len) return fail(PIRRT_E_RANGE, "best_path: capacity too small");
+    if (!path_out) return fail(PIRRT_E_INVAL, "best_path: NULL path_out");
+    for (int i = 0; i < len; ++i) path_out[i] = rev[len - 1 - i];
+    if (len_out) *len_out = len;
+    if (cost_out) *cost_out = gg;
+    return PIRRT_OK;
+}
+
+int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, const uint8_t* b) {
+    if (!c) return fail(PIRRT_E_INVAL, "set_policy: NULL context");
+    if (!parent || !g) return fail(PIRRT_E_INVAL, "set_policy: NULL array");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    cudaStream_t s = c->stream;
+    const int n = c->n;
+    const int* d_parent;
+    const double* d_g;
+    const unsigned char* d_b = nullptr;
+    // host-side canonicalisation of the snapshot: -0.0 -> +0.0, b -> {0,1}
+    std::vector<double> gh(g, g + n);
+    for (double& x : gh) x = x + 0.0;
+    std::vector<unsigned char> bh;
+    if (b) {
+        bh.resize(n);
+        for (int v = 0; v < n; ++v) bh[v] = b[v] ? 1 : 0;
+    }
+    if ((rc = stage(c, parent, n, false, c->s_parent, c->s_parent_cap, &d_parent))) return rc;
+    if ((rc = stage(c, (const double*)gh.data(), n, false, c->s_g, c->s_g_cap, &d_g))) return rc;
+    if (b && (rc = stage(c, (const unsigned char*)bh.data(), n, false, c->s_b, c->s_b_cap, &d_b))) return rc;
+    if ((rc = grow(c->s_pc, c->s_pc_cap, n, 0, s))) return rc;
+    CU(cudaMemsetAsync(c->s_pc, 0, (size_t)n * sizeof(double), s));
+    CU(cudaMemsetAsync(&c->ctl->err, 0, sizeof(int), s));
+    PolicyArgs a;
+    a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
+    a.doff = c->doff[c->cur]; a.didx = c->didx[c->cur]; a.dcost = c->dcost[c->cur];
+    a.parent_in = d_parent; a.g_in = d_g; a.b_in = d_b;
+    a.parent = nullptr; a.g = nullptr; a.pc = c->s_pc; a.b = nullptr;
+    a.n = n; a.ctl = c->ctl;
+    const long long l0 = g_kernel_launches;
+    CU(launch_set_policy(a, s));
+    c->launches += g_kernel_launches - l0;
+    if ((rc = read_ctl(c))) return rc;
+    if (c->ctl_host->err) {
+        const int err = c->ctl_host->err;
+        return fail((err & kErrRange) ? PIRRT_E_RANGE : PIRRT_E_INVAL, "set_policy rejected:" + err_bits(err));
+    }
+    // commit (g canonicalised: -0.0 -> +0.0 is irrelevant for validated g >= 0)
+    CU(cudaMemcpyAsync(c->parent, d_parent, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(c->g, d_g, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(c->pc, c->s_pc, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (d_b) {
+        CU(cudaMemcpyAsync(c->b, d_b, (size_t)n, cudaMemcpyDeviceToDevice, s));
+    } else {
+        CU(cudaMemsetAsync(c->b, 0, (size_t)n, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    return PIRRT_OK;
+}
+
+}  // extern "C"

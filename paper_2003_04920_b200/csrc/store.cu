@@ -1,0 +1,540 @@
+// store.cu -- the device-resident in-edge graph store and its append path
+// (row a1 of SURVEY.md section 8(a)).
+//
+// Layout: in-edge rows by destination vertex, stored
+// as a BASE CSR (boff i64[n+1], bidx i32[], bcost f64[]) plus a DELTA CSR of
+// the same shape holding every edge appended since the last compaction.
+// The paper rebuilds one CSR per Replan by radix sort + merge of the new
+// edges, O(|E|) per replan; here an append costs
+// O(n + |delta| + m) (counting-sort merge of the new edges into the delta)
+// and the delta is folded into the base when it exceeds a fraction of it
+// (geometric, amortised O(1) per edge).  Row order inside a row is not
+// significant: Improve takes a lexicographic (cost, id) minimum.
+//
+// Every kernel that writes committed state is gated on ctl->err == 0, and
+// the append path writes only locations that are invisible until the host
+// commits (the inactive delta buffers and vertex slots >= n_old), so a
+// rejected batch leaves the context unchanged.
+#include <cooperative_groups.h>
+
+#include <climits>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pirrt {
+namespace {
+
+constexpr int kBT = 256;      // block size of the plain kernels
+constexpr int kScanTile = 2048;
+
+inline int grid_for(long long n, int bt = kBT, int cap = 148 * 16) {
+    long long g = (n + bt - 1) / bt;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+__device__ __forceinline__ bool failed(const DevCtl* c) { return *(volatile const int*)&c->err != 0; }
+
+// ------------------------------------------------------------------ scan
+__global__ void k_scan_reduce(const long long* in, long long L, long long* part) {
+    __shared__ long long sm[kBT / 32];
+    const long long base = (long long)blockIdx.x * kScanTile;
+    long long s = 0;
+    for (int i = threadIdx.x; i < kScanTile; i += kBT) {
+        long long j = base + i;
+        if (j < L) s += in[j];
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < kBT / 32; ++w) t += sm[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+// single block: exclusive scan of the partials in place; part[P] = total
+__global__ void k_scan_partials(long long* part, long long P) {
+    __shared__ long long carry;
+    __shared__ long long sm[kBT / 32 + 1];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (long long base = 0; base < P; base += kBT) {
+        long long i = base + threadIdx.x;
+        long long x = i < P ? part[i] : 0;
+        long long inc = x;
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) sm[w] = inc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long r = 0;
+            for (int k = 0; k < kBT / 32; ++k) { long long t = sm[k]; sm[k] = r; r += t; }
+            sm[kBT / 32] = r;
+        }
+        __syncthreads();
+        if (i < P) part[i] = carry + sm[w] + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += sm[kBT / 32];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[P] = carry;
+}
+
+__global__ void k_scan_apply(const long long* in, long long L, const long long* part, long long* out) {
+    __shared__ long long sm[kBT / 32 + 1];
+    __shared__ long long carry;
+    const long long base = (long long)blockIdx.x * kScanTile;
+    if (threadIdx.x == 0) carry = part[blockIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int t = 0; t < kScanTile; t += kBT) {
+        long long i = base + t + threadIdx.x;
+        long long x = i < L ? in[i] : 0;
+        long long inc = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) sm[w] = inc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long r = 0;
+            for (int k = 0; k < kBT / 32; ++k) { long long q = sm[k]; sm[k] = r; r += q; }
+            sm[kBT / 32] = r;
+        }
+        __syncthreads();
+        if (i < L) out[i] = carry + sm[w] + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += sm[kBT / 32];
+        __syncthreads();
+    }
+}
+
+__global__ void k_set_ll(long long* p, long long v) { *p = v; }
+
+// ------------------------------------------------------------------ append
+// validation (R12): ids in range, no self-loop, finite non-negative cost/h
+__global__ void k_validate(const int* src, const int* dst, const double* cost, long long m,
+                           const double* h_in, const int* parent_in, const double* g_in,
+                           int n_old, int n_new, DevCtl* ctl) {
+    const long long n_all = (long long)n_old + n_new;
+    int err = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const int s = src[e], d = dst[e];
+        const double c = cost[e];
+        if (s < 0 || s >= n_all || d < 0 || d >= n_all) err |= kErrRange;
+        else if (s == d) err |= kErrSelfLoop;
+        if (!(c >= 0.0) || isinf(c)) err |= kErrCost;
+    }
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += stride) {
+        const double hv = h_in[i];
+        if (!(hv >= 0.0) || isinf(hv)) err |= kErrH;
+        if (parent_in) {
+            const int p = parent_in[i];
+            const double gv = g_in[i];
+            if (p < -1 || p >= n_all || p == n_old + i) err |= kErrRange;
+            else if (p < 0 && !isinf(gv)) err |= kErrGNew;
+            else if (p >= 0 && (!(gv >= 0.0) || isinf(gv))) err |= kErrGNew;
+        }
+    }
+    if (err) atomicOr(&ctl->err, err);
+}
+
+// cnt[v] = delta-row length of v before the append (0 for new vertices)
+__global__ void k_delta_count(const long long* doff_old, int n_old, int n_all, long long* cnt,
+                              const DevCtl* ctl) {
+    if (failed(ctl)) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n_all; v += gridDim.x * blockDim.x)
+        cnt[v] = (v < n_old) ? doff_old[v + 1] - doff_old[v] : 0;
+}
+
+__global__ void k_edge_hist(const int* src, const int* dst, long long m, int undirected,
+                            long long* cnt, const DevCtl* ctl) {
+    if (failed(ctl)) return;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        atomicAdd((unsigned long long*)&cnt[dst[e]], 1ull);
+        if (undirected) atomicAdd((unsigned long long*)&cnt[src[e]], 1ull);
+    }
+}
+
+// warp per row: copy the old delta row to its new position; leave the row's
+// write cursor in cnt[v]
+__global__ void k_delta_copy_old(const long long* doff_old, const int* didx_old,
+                                 const double* dcost_old, const long long* doff_new, int* didx_new,
+                                 double* dcost_new, int n_old, int n_all, long long* cursor,
+                                 const DevCtl* ctl) {
+    if (failed(ctl)) return;
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int v = w; v < n_all; v += nw) {
+        const long long dst0 = doff_new[v];
+        long long len = 0;
+        if (v < n_old) {
+            const long long s0 = doff_old[v], s1 = doff_old[v + 1];
+            len = s1 - s0;
+            for (long long k = lane; k < len; k += 32) {
+                didx_new[dst0 + k] = didx_old[s0 + k];
+                dcost_new[dst0 + k] = dcost_old[s0 + k];
+            }
+        }
+        if (lane == 0) cursor[v] = dst0 + len;
+    }
+}
+
+__global__ void k_delta_scatter(const int* src, const int* dst, const double* cost, long long m,
+                                int undirected, long long* cursor, int* didx_new,
+                                double* dcost_new, const DevCtl* ctl) {
+    if (failed(ctl)) return;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const int s = src[e], d = dst[e];
+        const double c = cost[e] + 0.0;   // -0.0 -> +0.0 (R12)
+        long long p = (long long)atomicAdd((unsigned long long*)&cursor[d], 1ull);
+        didx_new[p] = s;
+        dcost_new[p] = c;
+        if (undirected) {
+            p = (long long)atomicAdd((unsigned long long*)&cursor[s], 1ull);
+            didx_new[p] = d;
+            dcost_new[p] = c;
+        }
+    }
+}
+
+// base rows of the new vertices are empty: boff[v] = base_edges, v in (n_old, n_all]
+__global__ void k_base_extend(long long* boff, int n_old, int n_all, long long base_edges,
+                              const DevCtl* ctl) {
+    if (failed(ctl)) return;
+    for (int v = n_old + 1 + blockIdx.x * blockDim.x + threadIdx.x; v <= n_all;
+         v += gridDim.x * blockDim.x)
+        boff[v] = base_edges;
+}
+
+__global__ void k_init_new(const double* h_in, const int* parent_in, const double* g_in, int n_old,
+                           int n_new, double* g, double* h, int* parent, double* pc,
+                           unsigned char* b, const DevCtl* ctl) {
+    if (failed(ctl)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += gridDim.x * blockDim.x) {
+        const int v = n_old + i;
+        h[v] = h_in[i] + 0.0;
+        if (parent_in) {
+            parent[v] = parent_in[i];
+            g[v] = g_in[i] + 0.0;
+        } else {
+            parent[v] = -1;
+            g[v] = INFINITY;
+        }
+        pc[v] = 0.0;
+        b[v] = 0;
+    }
+}
+
+// warp per new vertex with a given parent: pc(v) = cost of the stored edge
+// (parent -> v); its absence is an error.  VALIDATE: g_new == g[p] + pc.
+__global__ void k_find_pc(const long long* boff, const int* bidx, const double* bcost,
+                          const long long* doff, const int* didx, const double* dcost,
+                          const int* parent, const double* g, double* pc, int v0, int v1,
+                          int validate, DevCtl* ctl) {
+    if (failed(ctl)) return;
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int v = v0 + w; v < v1; v += nw) {
+        const int p = parent[v];
+        if (p < 0) continue;
+        // the lowest stored position holding p (duplicates are the caller's problem)
+        long long best = LLONG_MAX;
+        double c = 0.0;
+        for (long long k = boff[v] + lane; k < boff[v + 1]; k += 32)
+            if (bidx[k] == p && k < best) { best = k; c = bcost[k]; }
+        for (long long k = doff[v] + lane; k < doff[v + 1]; k += 32)
+            if (didx[k] == p && (1LL << 62) + k < best) { best = (1LL << 62) + k; c = dcost[k]; }
+        for (int o = 16; o; o >>= 1) {
+            long long ob = __shfl_xor_sync(kFull, best, o);
+            double oc = __shfl_xor_sync(kFull, c, o);
+            if (ob < best) { best = ob; c = oc; }
+        }
+        if (lane == 0) {
+            if (best == LLONG_MAX) atomicOr(&ctl->err, kErrPcMissing);
+            else {
+                pc[v] = c;
+                if (validate && g[v] != g[p] + c) atomicOr(&ctl->err, kErrGNew);
+            }
+        }
+    }
+}
+
+// Extend's local relaxation of the new vertices (R14):
+// g(v) = lexicographic min over stored edges (u -> v), u < v, of
+// (g(u) + c, u).  Computed by chaotic (in-place) sweeps until a full sweep
+// changes no (g, parent) pair; since u < v along every dependency the fixed
+// point is unique and equals the sequential id-order result bit for bit.
+__global__ void __launch_bounds__(kBT) k_relax_new(
+    const long long* boff, const int* bidx, const double* bcost, const long long* doff,
+    const int* didx, const double* dcost, double* g, int* parent, double* pc, int n_old,
+    int n_new, DevCtl* ctl) {
+    cg::grid_group grid = cg::this_grid();
+    if (failed(ctl)) return;   // uniform: err is final before this kernel starts
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    for (int s = 0;; ++s) {
+        int* chg = &ctl->sweep_changed[s & 1];
+        if (lead) ctl->sweep_changed[(s + 1) & 1] = 0;
+        bool my_change = false;
+        for (int i = w; i < n_new; i += nw) {
+            const int v = n_old + i;
+            double best = INFINITY;
+            int arg = INT_MAX;
+            double argc = 0.0;
+            for (long long k = boff[v] + lane; k < boff[v + 1]; k += 32) {
+                const int u = bidx[k];
+                if (u >= v) continue;
+                const double c = bcost[k];
+                const double cand = *(volatile const double*)&g[u] + c;
+                if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
+            }
+            for (long long k = doff[v] + lane; k < doff[v + 1]; k += 32) {
+                const int u = didx[k];
+                if (u >= v) continue;
+                const double c = dcost[k];
+                const double cand = *(volatile const double*)&g[u] + c;
+                if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
+            }
+            double wb = best;
+            int wa = arg;
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, wb, o);
+                const int oa = __shfl_xor_sync(kFull, wa, o);
+                if (ob < wb || (ob == wb && oa < wa)) { wb = ob; wa = oa; }
+            }
+            const unsigned m = __ballot_sync(kFull, best == wb && arg == wa);
+            const double c = __shfl_sync(kFull, argc, __ffs(m) - 1);
+            if (lane == 0) {
+                int np;
+                double ng, npc;
+                if (wb < INFINITY) { np = wa; ng = wb; npc = c; }
+                else { np = -1; ng = INFINITY; npc = 0.0; }
+                if (np != parent[v] || __double_as_longlong(ng) != __double_as_longlong(g[v])) {
+                    *(volatile double*)&g[v] = ng;
+                    parent[v] = np;
+                    pc[v] = npc;
+                    my_change = true;
+                }
+            }
+        }
+        if (my_change) atomicOr(chg, 1);
+        grid.sync();
+        const int any = *(volatile int*)chg;
+        if (lead) ctl->sweeps = s + 1;
+        if (!any) break;
+        grid.sync();   // everyone has read chg before it is reset two sweeps later
+    }
+}
+
+// b(v) = g(v) + h(v) < g(x_goal) for the new vertices
+__global__ void k_new_promising(const double* g, const double* h, unsigned char* b, int n_old,
+                                int n_new, DevCtl* ctl) {
+    if (failed(ctl)) return;
+    const double thr = g[kGoal];
+    int cnt = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += gridDim.x * blockDim.x) {
+        const int v = n_old + i;
+        const unsigned char p = (g[v] + h[v] < thr) ? 1 : 0;
+        b[v] = p;
+        cnt += p;
+    }
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctl->nprom, cnt);
+}
+
+// ------------------------------------------------------------------ compaction
+__global__ void k_base_count(const long long* boff, const long long* doff, int n, long long* cnt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        cnt[v] = (boff[v + 1] - boff[v]) + (doff[v + 1] - doff[v]);
+}
+
+__global__ void k_base_merge(const long long* boff, const int* bidx, const double* bcost,
+                             const long long* doff, const int* didx, const double* dcost,
+                             const long long* boff_new, int* bidx_new, double* bcost_new, int n) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int v = w; v < n; v += nw) {
+        long long o = boff_new[v];
+        const long long b0 = boff[v], bl = boff[v + 1] - b0;
+        for (long long k = lane; k < bl; k += 32) {
+            bidx_new[o + k] = bidx[b0 + k];
+            bcost_new[o + k] = bcost[b0 + k];
+        }
+        o += bl;
+        const long long d0 = doff[v], dl = doff[v + 1] - d0;
+        for (long long k = lane; k < dl; k += 32) {
+            bidx_new[o + k] = didx[d0 + k];
+            bcost_new[o + k] = dcost[d0 + k];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ policy
+// validate a policy snapshot (no writes: the host commits after the check)
+__global__ void k_check_policy(const int* parent_in, const double* g_in, int n, DevCtl* ctl) {
+    int err = 0;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int p = parent_in[v];
+        const double gv = g_in[v];
+        if (p < -1 || p >= n || p == v) err |= kErrRange;
+        if (!(gv >= 0.0)) err |= kErrGNew;
+        if (v == kRoot && (p != -1 || gv != 0.0)) err |= kErrRoot;
+    }
+    if (err) atomicOr(&ctl->err, err);
+}
+
+__global__ void k_best_path(const int* parent, int n, int* path_rev, int* len_out) {
+    int v = kGoal, len = 0;
+    while (v != -1 && len <= n) {
+        path_rev[len++] = v;
+        v = parent[v];
+    }
+    *len_out = (v == -1) ? len : -1;   // -1: cycle
+}
+
+}  // namespace
+
+thread_local long long g_kernel_launches = 0;
+
+size_t scan_tmp_elems(long long L) { return (size_t)((L + kScanTile - 1) / kScanTile + 2); }
+
+cudaError_t scan_exclusive(const long long* in, long long* out, long long L, long long* tmp,
+                           cudaStream_t s) {
+    if (L <= 0) {
+        ++g_kernel_launches;
+        k_set_ll<<<1, 1, 0, s>>>(out, 0);
+        return cudaGetLastError();
+    }
+    const long long P = (L + kScanTile - 1) / kScanTile;
+    ++g_kernel_launches;
+    k_scan_reduce<<<(unsigned)P, kBT, 0, s>>>(in, L, tmp);
+    ++g_kernel_launches;
+    k_scan_partials<<<1, kBT, 0, s>>>(tmp, P);
+    ++g_kernel_launches;
+    k_scan_apply<<<(unsigned)P, kBT, 0, s>>>(in, L, tmp, out);
+    // out[L] = total = tmp[P]
+    cudaMemcpyAsync(out + L, tmp + P, sizeof(long long), cudaMemcpyDeviceToDevice, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
+    const int n_all = a.n_old + a.n_new;
+    const long long m = a.m;
+    cudaError_t e;
+    // 1. validation
+    {
+        long long work = m > a.n_new ? m : a.n_new;
+        ++g_kernel_launches;
+        k_validate<<<grid_for(work), kBT, 0, s>>>(a.src, a.dst, a.cost, m, a.h_in, a.parent_in,
+                                                  a.g_in, a.n_old, a.n_new, a.ctl);
+    }
+    // 2. delta merge (counting sort of the new edges by destination)
+    ++g_kernel_launches;
+    k_delta_count<<<grid_for(n_all + 1), kBT, 0, s>>>(a.doff_old, a.n_old, n_all, a.cnt, a.ctl);
+    if (m > 0) {
+        ++g_kernel_launches;
+        k_edge_hist<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, m, a.undirected, a.cnt, a.ctl);
+    }
+    if ((e = scan_exclusive(a.cnt, a.doff_new, n_all, a.scan_tmp, s)) != cudaSuccess) return e;
+    ++g_kernel_launches;
+    k_delta_copy_old<<<grid_for((long long)n_all * 32), kBT, 0, s>>>(
+        a.doff_old, a.didx_old, a.dcost_old, a.doff_new, a.didx_new, a.dcost_new, a.n_old, n_all,
+        a.cnt, a.ctl);
+    if (m > 0) {
+        ++g_kernel_launches;
+        k_delta_scatter<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, a.cost, m, a.undirected, a.cnt,
+                                                    a.didx_new, a.dcost_new, a.ctl);
+    }
+    ++g_kernel_launches;
+    k_base_extend<<<grid_for(a.n_new + 1), kBT, 0, s>>>(a.boff_w, a.n_old, n_all, a.base_edges,
+                                                        a.ctl);
+    // 3. new vertex state
+    if (a.n_new > 0) {
+        ++g_kernel_launches;
+        k_init_new<<<grid_for(a.n_new), kBT, 0, s>>>(a.h_in, a.parent_in, a.g_in, a.n_old, a.n_new,
+                                                     a.g, a.h, a.parent, a.pc, a.b, a.ctl);
+        if (a.parent_in) {
+            ++g_kernel_launches;
+            k_find_pc<<<grid_for((long long)a.n_new * 32), kBT, 0, s>>>(
+                a.boff, a.bidx, a.bcost, a.doff_new, a.didx_new, a.dcost_new, a.parent, a.g, a.pc,
+                a.n_old, n_all, a.validate, a.ctl);
+        } else {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_relax_new, kBT, 0);
+            long long want = ((long long)a.n_new * 32 + kBT - 1) / kBT;
+            long long maxb = (long long)per_sm * (a.grid_blocks > 0 ? a.grid_blocks : 148);
+            int blocks = (int)(want < maxb ? want : maxb);
+            if (blocks < 1) blocks = 1;
+            const long long* boff = a.boff;
+            const int* bidx = a.bidx;
+            const double* bcost = a.bcost;
+            const long long* doff = a.doff_new;
+            const int* didx = a.didx_new;
+            const double* dcost = a.dcost_new;
+            double* g = a.g;
+            int* parent = a.parent;
+            double* pc = a.pc;
+            int n_old = a.n_old, n_new = a.n_new;
+            DevCtl* ctl = a.ctl;
+            void* params[] = {&boff, &bidx, &bcost, &doff, &didx, &dcost, &g, &parent, &pc,
+                              &n_old, &n_new, &ctl};
+            ++g_kernel_launches;
+            if ((e = cudaLaunchCooperativeKernel((const void*)k_relax_new, dim3(blocks), dim3(kBT),
+                                                 params, 0, s)) != cudaSuccess)
+                return e;
+        }
+        ++g_kernel_launches;
+        k_new_promising<<<grid_for(a.n_new), kBT, 0, s>>>(a.g, a.h, a.b, a.n_old, a.n_new, a.ctl);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
+    cudaError_t e;
+    ++g_kernel_launches;
+    k_base_count<<<grid_for(a.n), kBT, 0, s>>>(a.boff, a.doff, a.n, a.cnt);
+    if ((e = scan_exclusive(a.cnt, a.boff_new, a.n, a.scan_tmp, s)) != cudaSuccess) return e;
+    ++g_kernel_launches;
+    k_base_merge<<<grid_for((long long)a.n * 32), kBT, 0, s>>>(
+        a.boff, a.bidx, a.bcost, a.doff, a.didx, a.dcost, a.boff_new, a.bidx_new, a.bcost_new, a.n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_policy(const PolicyArgs& a, cudaStream_t s) {
+    // a.parent/a.g/a.pc are STAGING arrays here; the caller commits them
+    ++g_kernel_launches;
+    k_check_policy<<<grid_for(a.n), kBT, 0, s>>>(a.parent_in, a.g_in, a.n, a.ctl);
+    ++g_kernel_launches;
+    k_find_pc<<<grid_for((long long)a.n * 32), kBT, 0, s>>>(a.boff, a.bidx, a.bcost, a.doff, a.didx,
+                                                            a.dcost, a.parent_in, a.g_in, a.pc, 0,
+                                                            a.n, 0, a.ctl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_best_path(const int* parent, int n, int* path_rev, int* len_out,
+                             cudaStream_t s) {
+    ++g_kernel_launches;
+    k_best_path<<<1, 1, 0, s>>>(parent, n, path_rev, len_out);
+    return cudaGetLastError();
+}
+
+}  // namespace pirrt

@@ -1,0 +1,276 @@
+"""Thin ctypes binding of the C ABI in include/pirrt.h (libpirrt.so).
+
+Argument marshalling only: every step of the exploitation path runs in the
+CUDA kernels of ``csrc/``.  Importing this module loads the in-tree
+``lib/libpirrt.so`` and raises ImportError if it is missing -- there is no
+CPU fallback.
+
+Functions keep the ABI names (``pirrt_create``, ``pirrt_graph_append_batch``,
+``pirrt_exploit``, ``pirrt_get_policy``, ``pirrt_get_costs``,
+``pirrt_best_path`` ...); :class:`Context` wraps them for numpy arrays (host
+pointers) and torch CUDA tensors (``PIRRT_F_DEVICE_PTRS``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpirrt.so")
+
+PIRRT_OK = 0
+PIRRT_E_INVAL = -1
+PIRRT_E_RANGE = -2
+PIRRT_E_NOMEM = -3
+PIRRT_E_CUDA = -4
+PIRRT_E_NCCL = -5
+PIRRT_E_NOCONV = -6
+PIRRT_E_STATE = -7
+PIRRT_E_CORRUPT = -8
+
+PIRRT_F_PRUNE_OFF = 1
+PIRRT_F_VALIDATE = 2
+PIRRT_F_EDGES_UNDIRECTED = 4
+PIRRT_F_DEVICE_PTRS = 8
+
+# every symbol include/pirrt.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "pirrt_config_init", "pirrt_create", "pirrt_destroy", "pirrt_graph_append_batch",
+    "pirrt_exploit", "pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
+    "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
+    "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error",
+)
+
+
+class pirrt_config(C.Structure):
+    _fields_ = [
+        ("vertex_capacity", C.c_int64),
+        ("edge_capacity", C.c_int64),
+        ("h_root", C.c_double),
+        ("h_goal", C.c_double),
+        ("epsilon", C.c_double),
+        ("max_iterations", C.c_int32),
+        ("flags", C.c_uint32),
+        ("device", C.c_int32),
+        ("stream", C.c_void_p),
+        ("grid_blocks", C.c_int32),
+        ("nranks", C.c_int32),
+        ("rank", C.c_int32),
+        ("nccl_unique_id", C.c_void_p),
+    ]
+
+
+class pirrt_exploit_stats(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32),
+        ("evaluations", C.c_int32),
+        ("last_delta_g", C.c_double),
+        ("relaxations", C.c_int64),
+        ("eval_visits", C.c_int64),
+        ("max_level", C.c_int32),
+        ("promising", C.c_int32),
+        ("stalled", C.c_int32),
+        ("grid_blocks", C.c_int32),
+        ("device_ms", C.c_float),
+        ("improve_ms", C.c_float),
+        ("evaluate_ms", C.c_float),
+        ("compact_ms", C.c_float),
+        ("improve_set", C.c_int64),
+        ("children_index", C.c_int64),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `make cuda` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    lib.pirrt_config_init.argtypes = [C.POINTER(pirrt_config)]
+    lib.pirrt_config_init.restype = None
+    lib.pirrt_create.argtypes = [C.POINTER(pirrt_config), C.POINTER(C.c_void_p)]
+    lib.pirrt_destroy.argtypes = [P]
+    lib.pirrt_graph_append_batch.argtypes = [P, C.c_int32, P, P, P, C.c_int64, P, P, P,
+                                             C.c_uint32, P]
+    lib.pirrt_exploit.argtypes = [P, C.POINTER(pirrt_exploit_stats)]
+    for f in ("pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
+              "pirrt_get_parent_costs"):
+        getattr(lib, f).argtypes = [P, P, C.c_int64]
+    lib.pirrt_best_path.argtypes = [P, P, C.c_int64, P, P]
+    lib.pirrt_set_policy.argtypes = [P, P, P, P]
+    lib.pirrt_num_vertices.argtypes = [P]
+    lib.pirrt_num_vertices.restype = C.c_int64
+    lib.pirrt_num_edges.argtypes = [P]
+    lib.pirrt_num_edges.restype = C.c_int64
+    lib.pirrt_kernel_launches.argtypes = [P]
+    lib.pirrt_kernel_launches.restype = C.c_int64
+    lib.pirrt_last_error.restype = C.c_char_p
+    return lib
+
+
+_lib = _load()
+
+# ABI-named entry points (same names as include/pirrt.h)
+pirrt_config_init = _lib.pirrt_config_init
+pirrt_create = _lib.pirrt_create
+pirrt_destroy = _lib.pirrt_destroy
+pirrt_graph_append_batch = _lib.pirrt_graph_append_batch
+pirrt_exploit = _lib.pirrt_exploit
+pirrt_get_policy = _lib.pirrt_get_policy
+pirrt_get_costs = _lib.pirrt_get_costs
+pirrt_get_promising = _lib.pirrt_get_promising
+pirrt_get_parent_costs = _lib.pirrt_get_parent_costs
+pirrt_best_path = _lib.pirrt_best_path
+pirrt_set_policy = _lib.pirrt_set_policy
+pirrt_num_vertices = _lib.pirrt_num_vertices
+pirrt_num_edges = _lib.pirrt_num_edges
+pirrt_kernel_launches = _lib.pirrt_kernel_launches
+pirrt_last_error = _lib.pirrt_last_error
+
+
+class PirrtError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"pirrt error {code}: {msg}")
+        self.code = code
+
+
+def _check(rc: int):
+    if rc != PIRRT_OK:
+        raise PirrtError(rc, (_lib.pirrt_last_error() or b"").decode())
+
+
+@dataclass
+class ExploitStats:
+    iterations: int
+    evaluations: int
+    last_delta_g: float
+    relaxations: int
+    eval_visits: int
+    max_level: int
+    promising: int
+    stalled: int
+    grid_blocks: int
+    device_ms: float
+    improve_ms: float
+    evaluate_ms: float
+    compact_ms: float
+    improve_set: int
+    children_index: int
+
+
+def _is_torch_cuda(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+class Context:
+    """One exploitation context (vertices 0 = x_init and 1 = x_goal exist)."""
+
+    def __init__(self, h_root=0.0, h_goal=0.0, epsilon=0.0, max_iterations=0, flags=0, device=0,
+                 stream=None, vertex_capacity=0, edge_capacity=0, grid_blocks=0):
+        cfg = pirrt_config()
+        pirrt_config_init(C.byref(cfg))
+        cfg.h_root, cfg.h_goal, cfg.epsilon = float(h_root), float(h_goal), float(epsilon)
+        cfg.max_iterations, cfg.flags, cfg.device = int(max_iterations), int(flags), int(device)
+        cfg.vertex_capacity, cfg.edge_capacity = int(vertex_capacity), int(edge_capacity)
+        cfg.grid_blocks = int(grid_blocks)
+        if stream is not None:
+            cfg.stream = int(getattr(stream, "cuda_stream", stream))
+        h = C.c_void_p()
+        _check(pirrt_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self.cfg = cfg
+
+    def close(self):
+        if getattr(self, "_h", None):
+            pirrt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n(self) -> int:
+        return int(pirrt_num_vertices(self._h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(pirrt_kernel_launches(self._h))
+
+    @property
+    def n_edges(self) -> int:
+        return int(pirrt_num_edges(self._h))
+
+    def append(self, h_new, src, dst, cost, parent_new=None, g_new=None, flags=0) -> int:
+        """pirrt_graph_append_batch.  numpy arrays -> host pointers; torch CUDA
+        tensors (all of them) -> PIRRT_F_DEVICE_PTRS."""
+        if _is_torch_cuda(h_new) or _is_torch_cuda(src):
+            flags |= PIRRT_F_DEVICE_PTRS
+            ptr = lambda t: None if t is None else t.data_ptr()
+            nn, m = int(h_new.numel()), int(src.numel())
+            keep = ()
+        else:
+            h_new = np.ascontiguousarray(h_new, np.float64)
+            src = np.ascontiguousarray(src, np.int32)
+            dst = np.ascontiguousarray(dst, np.int32)
+            cost = np.ascontiguousarray(cost, np.float64)
+            if parent_new is not None:
+                parent_new = np.ascontiguousarray(parent_new, np.int32)
+                g_new = np.ascontiguousarray(g_new, np.float64)
+            ptr = lambda a: None if a is None else (a.ctypes.data if a.size else None)
+            nn, m = int(h_new.size), int(src.size)
+            keep = (h_new, src, dst, cost, parent_new, g_new)
+        out = C.c_int32(0)
+        _check(pirrt_graph_append_batch(self._h, nn, ptr(h_new), ptr(parent_new), ptr(g_new), m,
+                                        ptr(src), ptr(dst), ptr(cost), int(flags), C.byref(out)))
+        del keep
+        return int(out.value)
+
+    def exploit(self) -> ExploitStats:
+        st = pirrt_exploit_stats()
+        _check(pirrt_exploit(self._h, C.byref(st)))
+        return ExploitStats(*(getattr(st, f[0]) for f in pirrt_exploit_stats._fields_))
+
+    def _get(self, fn, dtype):
+        n = self.n
+        out = np.empty(n, dtype)
+        _check(fn(self._h, out.ctypes.data, n))
+        return out
+
+    def policy(self):
+        return self._get(pirrt_get_policy, np.int32)
+
+    def costs(self):
+        return self._get(pirrt_get_costs, np.float64)
+
+    def promising(self):
+        return self._get(pirrt_get_promising, np.uint8)
+
+    def parent_costs(self):
+        return self._get(pirrt_get_parent_costs, np.float64)
+
+    def state(self):
+        """(parent, g, pc, b) -- same order as the oracle's state()."""
+        return self.policy(), self.costs(), self.parent_costs(), self.promising()
+
+    def best_path(self):
+        cap = max(self.n, 1)
+        path = np.empty(cap, np.int32)
+        ln = C.c_int64(0)
+        cost = C.c_double(0)
+        _check(pirrt_best_path(self._h, path.ctypes.data, cap, C.byref(ln), C.byref(cost)))
+        return path[: ln.value].copy(), float(cost.value)
+
+    def set_policy(self, parent, g, b=None):
+        parent = np.ascontiguousarray(parent, np.int32)
+        g = np.ascontiguousarray(g, np.float64)
+        bp = None
+        if b is not None:
+            b = np.ascontiguousarray(b, np.uint8)
+            bp = b.ctypes.data
+        _check(pirrt_set_policy(self._h, parent.ctypes.data, g.ctypes.data, bp))

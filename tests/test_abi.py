@@ -1,0 +1,67 @@
+"""CPU-side checks of the C-ABI library: it loads and exports every symbol
+include/pirrt.h declares, and the Python binding's struct layouts match the
+header (no compute calls: there is no GPU here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pirrt.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pirrt_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_expected_calls():
+    names = declared_functions()
+    # SURVEY.md section 8(b) boundary calls
+    for must in ("pirrt_graph_append_batch", "pirrt_exploit", "pirrt_get_policy",
+                 "pirrt_get_costs", "pirrt_best_path"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2003_04920_b200 import pirrt
+    lib = C.CDLL(pirrt.LIB_PATH)
+    names = declared_functions()
+    assert sorted(pirrt.EXPORTS) == names
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_struct_layouts_match_header():
+    from paper_2003_04920_b200 import pirrt
+    # sizes computed from the C declarations (x86-64 / aarch64 LP64 ABI)
+    assert C.sizeof(pirrt.pirrt_config) == 8 + 8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 8 + 4 + 4 + 4 + 4 + 8
+    assert C.sizeof(pirrt.pirrt_exploit_stats) == 4 + 4 + 8 + 8 + 8 + 4 * 4 + 4 * 4 + 8 + 8
+    cfg = pirrt.pirrt_config()
+    pirrt.pirrt_config_init(C.byref(cfg))
+    assert cfg.nranks == 1 and cfg.epsilon == 0.0 and cfg.flags == 0
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "pirrt_copy", os.path.join(ROOT, "paper_2003_04920_b200", "pirrt.py"))
+    mod = importlib.util.module_from_spec(spec)
+    # point the copy at an empty directory: import must raise, not fall back
+    src = open(spec.origin).read().replace(
+        'LIB_PATH = os.path.join(_HERE, "lib", "libpirrt.so")',
+        f'LIB_PATH = {str(tmp_path / "libpirrt.so")!r}')
+    with pytest.raises(ImportError):
+        exec(compile(src, spec.origin, "exec"), mod.__dict__)
+
+
+def test_so_is_sm100a():
+    from paper_2003_04920_b200 import pirrt
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", pirrt.LIB_PATH],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
