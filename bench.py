@@ -1,0 +1,493 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 PI-RRT# exploitation library.
+
+Workload (BASELINE.json north_star target, configs[2]): a 6-D random
+geometric graph with box obstacles and the incremental radius
+r(m) = gamma (ln m / m)^(1/6), grown by BE-RRT# batches of S samples
+(Alg. 3) to 1,000,000 vertices.  One STEP is one pass of
+the whole hot path over one batch:
+pirrt_graph_append_batch (a1, incl. local relaxation) -> pirrt_exploit
+(a2-a5, converged policy iteration; skipped only by the Alg. 3 guard) ->
+pirrt_best_path (a6).  The device leg (`value`) times the W warm-up + K timed
+batches that end exactly at vertex 1,000,000, with the batch inputs already
+resident in HBM; the e2e leg times the next W + K batches through the same
+C ABI from pinned HOST buffers (H2D/D2H inside the timed region).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
+Under torchrun (N > 1) every rank runs an independent replica (weak scaling,
+DESIGN.md section 7); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per converged PI exploitation + edge relaxations/s (GTEPS) vs gather roofline"
+
+# algorithmic bytes per unit of work
+B_RELAX = 20.0      # idx i32 + cost f64 streamed (12 B) + g[u] gather (8 B)
+B_IVERT = 40.0      # Improve vertex: 4 row offsets (32 B) + g[v] (8 B)
+B_VISIT = 37.0      # Evaluate visit: parent 4, pc 8, g[p] 8, g write 8, h 8, b 1
+B_KIDX = 16.0       # children index per vertex per Evaluate: parent 4, count 4, rank 4, kids 4
+B_COMPACT = 1.0     # promising flag per vertex per iteration
+
+
+def algo_bytes(st, n):
+    return (st.relaxations * B_RELAX + st.improve_set * B_IVERT + st.eval_visits * B_VISIT
+            + st.children_index * B_KIDX + st.iterations * n * B_COMPACT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
+    ap.add_argument("--d", type=int, default=6)
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--S", type=int, default=4096)
+    ap.add_argument("--gamma", choices=["k", "star"], default="k")
+    ap.add_argument("--boxes", type=int, default=20)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--graph-cache", default="", help="npz path to reuse a generated graph")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return f"cfg3_{a.d}d_{a.n // 1000}k_berrt_S{a.S}_gamma{a.gamma}_{a.boxes}boxes"
+
+
+# ------------------------------------------------------------------ inputs
+
+def make_graph(a, rank, world):
+    """Generate (rank 0) or load (other ranks) the seeded RRG."""
+    import gen
+    gm = gen.gamma_k(a.d) if a.gamma == "k" else gen.gamma_star(a.d)
+    n_total = a.n + (a.warmup + a.steps) * a.S
+    seed = gen.seed_of(workload_name(a), a.seed)
+    shm = f"/dev/shm/pirrt_bench_{os.getpid() if world == 1 else os.environ.get('MASTER_PORT', '0')}.npz"
+    t0 = time.perf_counter()
+    cache = a.graph_cache
+    if cache and os.path.exists(cache) and (world == 1 or rank == 0):
+        # the generator is prefix-stable (vertex i's edges depend only on
+        # points <= i), so a cached graph with at least n_total vertices serves
+        z = np.load(cache)
+        g = gen.RRG(a.d, int(z["h"].size), gm, z["points"], z["boxes"], z["h"], z["off"],
+                    z["nbr"], z["cost"], int(z["meta"][0]), int(z["meta"][1]))
+        assert int(z["meta"][2]) == seed and g.n >= n_total, "stale graph cache"
+    elif world == 1 or rank == 0:
+        threads = max(1, (os.cpu_count() or 1))
+        g = gen.rrg(a.d, n_total, gm, n_boxes=a.boxes, seed=seed, threads=threads)
+        if cache:
+            np.savez(cache, points=g.points, boxes=g.boxes, h=g.h, off=g.off, nbr=g.nbr,
+                     cost=g.cost, meta=np.array([g.n_isolated, g.n_candidates, seed], np.uint64))
+    if world == 1 or rank == 0:
+        if world > 1:
+            np.savez(shm, points=g.points, boxes=g.boxes, h=g.h, off=g.off, nbr=g.nbr,
+                     cost=g.cost, meta=np.array([g.n_isolated, g.n_candidates]))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        if rank != 0:
+            z = np.load(shm)
+            g = gen.RRG(a.d, n_total, gm, z["points"], z["boxes"], z["h"], z["off"], z["nbr"],
+                        z["cost"], int(z["meta"][0]), int(z["meta"][1]))
+        dist.barrier()
+        if rank == 0:
+            try:
+                os.unlink(shm)
+            except OSError:
+                pass
+    return g, gm, time.perf_counter() - t0
+
+
+def legs(a):
+    """Vertex ranges: pre-load [2, p0); device leg W+K batches ending at n;
+    e2e leg W+K batches after n."""
+    S, W, K = a.S, a.warmup, a.steps
+    dev0 = a.n - (W + K) * S
+    dev = [(dev0 + i * S, dev0 + (i + 1) * S) for i in range(W + K)]
+    e2e = [(a.n + i * S, a.n + (i + 1) * S) for i in range(W + K)]
+    return dev0, dev, e2e
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = f"/tmp/pirrt_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0])); smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        try:
+            os.unlink(self.path)
+        except OSError:
+            pass
+        busy = [x for x in sm if x > 300] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ legs
+
+def run_cuda(a, rank, world):
+    import torch
+    from paper_2003_04920_b200 import pirrt
+    from paper_2003_04920_b200.berrt import EDGES_UNDIRECTED, replay
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    g, gm, t_gen = make_graph(a, rank, world)
+    dev0, dev_batches, e2e_batches = legs(a)
+    stream = torch.cuda.current_stream()
+    ctx = pirrt.Context(h_root=g.h_root(), stream=stream, vertex_capacity=g.n + 1024,
+                        edge_capacity=int(2.4 * g.off[-1]) + 4096)
+    # ---- pre-load: BE-RRT# history up to dev0 (untimed)
+    t0 = time.perf_counter()
+    replay(ctx, g, a.S, n_stop=dev0, final=False)
+    t_pre = time.perf_counter() - t0
+    # ---- inputs of the device leg resident in HBM before timing
+    def to_dev(x):
+        return torch.from_numpy(np.ascontiguousarray(x)).to(f"cuda:{dev}")
+    dev_in = []
+    for (lo, hi) in dev_batches:
+        s, d_, c = g.batch(lo, hi, directed=False)
+        dev_in.append((to_dev(g.h[lo:hi]), to_dev(s), to_dev(d_), to_dev(c)))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.warmup + a.steps)]
+    clocks = ClockSampler(dev)
+    clocks.start()
+
+    def step(inputs):
+        nprom = ctx.append(*inputs, flags=EDGES_UNDIRECTED)
+        st = ctx.exploit() if nprom > 0 else None            # Alg. 3 guard (R10)
+        path, cost = ctx.best_path()
+        return st, nprom, path
+
+    stats = []
+    for i in range(a.warmup):
+        flush.zero_()
+        step(dev_in[i])
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.kernel_launches
+    torch.cuda.nvtx.range_push("timed")
+    wall0 = time.perf_counter()
+    for i in range(a.warmup, a.warmup + a.steps):
+        flush.zero_()                                          # L2 flush between timed steps
+        e0, e1 = ev[i]
+        e0.record(stream)
+        st, nprom, path = step(dev_in[i])
+        e1.record(stream)
+        stats.append(st)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    torch.cuda.nvtx.range_pop()
+    launches = ctx.kernel_launches - l0
+    step_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(a.warmup, a.warmup + a.steps)]
+    total_ms = float(sum(step_ms))
+    # ---- e2e leg: same ABI from pinned host buffers
+    host_in = []
+    for (lo, hi) in e2e_batches:
+        s, d_, c = g.batch(lo, hi, directed=False)
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+        host_in.append((pin(g.h[lo:hi]), pin(s), pin(d_), pin(c)))
+    h2d = d2h = 0
+    e2e_ms = []
+    import ctypes
+    for i in range(a.warmup + a.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st, nprom, path = step(host_in[i])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= a.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+            h2d += sum(x.nbytes for x in host_in[i])
+            d2h += 4 + path.nbytes + 16 + (ctypes.sizeof(pirrt.pirrt_exploit_stats) if st else 0)
+    clk = clocks.stop()
+    ex = [s for s in stats if s is not None]
+    relax = sum(s.relaxations for s in ex)
+    ex_ms = sum(s.device_ms for s in ex)
+    bytes_ = sum(algo_bytes(s, a.n) for s in ex)
+    res = {
+        "total_ms": total_ms, "step_ms": step_ms, "wall_s": wall, "launches": launches,
+        "relax": relax, "exploit_ms": ex_ms, "bytes": bytes_, "n_exploits": len(ex),
+        "e2e_ms": float(sum(e2e_ms)), "h2d": h2d / a.steps, "d2h": d2h / a.steps,
+        "clocks": clk, "t_gen": t_gen, "t_pre": t_pre,
+        "iters": [s.iterations for s in ex], "prom": [s.promising for s in ex],
+        "improve_ms": sum(s.improve_ms for s in ex), "evaluate_ms": sum(s.evaluate_ms for s in ex),
+        "compact_ms": sum(s.compact_ms for s in ex),
+        "improve_bytes": sum(s.relaxations * B_RELAX + s.improve_set * B_IVERT for s in ex),
+        "max_level": max([s.max_level for s in ex] or [0]),
+        "graph": {"n_total": g.n, "pairs": g.n_pairs, "mean_degree": g.mean_degree,
+                  "isolated": g.n_isolated, "gamma": gm},
+        "edges_stored": ctx.n_edges, "n_at_end_of_device_leg": a.n,
+    }
+    return res, g, gm
+
+
+def oracle_leg(a, g, batches, budget_s, p0):
+    """Time the serial oracle on a bounded sample of the same workload.
+
+    The oracle builds its own state (no input from the CUDA path): vertices
+    [2, p0) appended as one batch and exploited (untimed), then the given
+    S-batches are timed one by one (append + exploit + best_path) until the
+    budget is spent."""
+    from oracle import EDGES_UNDIRECTED, Oracle
+    o = Oracle(h_root=g.h_root())
+    t0 = time.perf_counter()
+    s, d_, c = g.batch(2, p0, directed=False)
+    o.append(g.h[2:p0], s, d_, c, flags=EDGES_UNDIRECTED)
+    o.exploit()
+    t_setup = time.perf_counter() - t0
+    times, relax = [], 0
+    spent = 0.0
+    for (lo, hi) in batches:
+        s, d_, c = g.batch(lo, hi, directed=False)
+        t = time.perf_counter()
+        nprom = o.append(g.h[lo:hi], s, d_, c, flags=EDGES_UNDIRECTED)
+        st = o.exploit() if nprom > 0 else None
+        o.best_path()
+        dt = time.perf_counter() - t
+        times.append(dt)
+        relax += st.relaxations if st else 0
+        spent += dt
+        if spent > budget_s:
+            break
+    return times, relax, t_setup
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_per_launch():
+    p = os.path.join(ROOT, "profiles", "exploit_ncu_summary.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if a.impl == "reference":
+        return main_reference(a, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    res, g, gm = run_cuda(a, rank, world)
+    total_ms, relax, e2e_ms = res["total_ms"], res["relax"], res["e2e_ms"]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        r = torch.tensor([float(relax)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(r, op=dist.ReduceOp.SUM)
+        total_ms, e2e_ms, relax_all = float(t[0]), float(t[1]), float(r[0])
+    else:
+        relax_all = float(relax)
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    ms_step = total_ms / a.steps
+    peak, peak_src = peaks()
+    achieved = res["bytes"] / (res["exploit_ms"] * 1e-3) / 1e9 if res["exploit_ms"] > 0 else 0.0
+    line = {
+        "metric": METRIC,
+        "value": round(ms_step, 4),
+        "unit": "ms",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": workload_name(a),
+            "d": a.d, "n": a.n, "S": a.S, "gamma": a.gamma, "gamma_value": round(gm, 6),
+            "boxes": a.boxes, "mean_degree": round(res["graph"]["mean_degree"], 3),
+            "directed_edges_stored": res["edges_stored"],
+            "step": "append(S, device ptrs) + exploit-to-convergence + best_path",
+            "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": "single" if world == 1 else f"replicas{world}",
+        },
+        "gteps": round(relax_all / (total_ms * 1e-3) / 1e9, 4),
+        "exploit_ms_mean": round(res["exploit_ms"] / max(1, res["n_exploits"]), 4),
+        "exploit_gteps": round(res["relax"] / (res["exploit_ms"] * 1e-3) / 1e9, 4) if res["exploit_ms"] else 0,
+        "append_plus_readout_ms_mean": round((res["total_ms"] - res["exploit_ms"]) / a.steps, 4),
+        "iterations_mean": round(statistics.mean(res["iters"]), 3) if res["iters"] else 0,
+        "promising_mean": round(statistics.mean(res["prom"]), 1) if res["prom"] else 0,
+        "relaxations_per_step": round(res["relax"] / a.steps),
+        "max_level": res["max_level"],
+        "phase_ms": {"compact": round(res["compact_ms"], 4), "improve": round(res["improve_ms"], 4),
+                     "evaluate": round(res["evaluate_ms"], 4)},
+        "roofline": {
+            "kernel": "exploit_kernel (persistent: compaction+Improve+Evaluate)",
+            "bound": "hbm",
+            "achieved": round(achieved, 2),
+            "peak": peak,
+            "peak_source": peak_src,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 5),
+            "traffic": traffic_per_launch(),
+            "algorithmic_bytes_per_launch": round(res["bytes"] / max(1, res["n_exploits"])),
+            "improve_phase_GBps": round(res["improve_bytes"] / (res["improve_ms"] * 1e-3) / 1e9, 2)
+            if res["improve_ms"] > 0 else None,
+        },
+        "e2e": {"value": round(e2e_ms / a.steps, 4), "unit": "ms",
+                "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"])},
+        "gpu_launches": int(res["launches"]),
+        "clocks": res["clocks"],
+        "setup_s": {"generate": round(res["t_gen"], 2), "preload_replay": round(res["t_pre"], 2)},
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        dev0, dev_batches, _ = legs(a)
+        times, orelax, t_setup = oracle_leg(a, g, dev_batches, a.cpu_budget_s, dev0)
+        model, ncpu = cpu_info()
+        line["cpu_baseline"] = {
+            "value": round(1e3 * statistics.mean(times), 3), "unit": "ms", "cores": 1,
+            "kind": "oracle",
+            "sample": f"{len(times)} S={a.S} steps (append+exploit+best_path) of the same graph "
+                      f"after the oracle built its own state at n={dev0} (one batch + exploit, "
+                      f"{t_setup:.1f}s untimed); serial oracle on 1 of {ncpu} host cores ({model})",
+        }
+    else:
+        line["cpu_baseline"] = None
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main_reference(a, rank, world):
+    """--impl reference: the oracle (the only reference this tier has), timed
+    on the host cores on the same workload; rank 0 only."""
+    if rank != 0:
+        return
+    g, gm, _ = make_graph(a, 0, 1)
+    dev0, dev_batches, _ = legs(a)
+    from oracle import EDGES_UNDIRECTED, Oracle
+    o = Oracle(h_root=g.h_root())
+    t0 = time.perf_counter()
+    s, d_, c = g.batch(2, dev0, directed=False)
+    o.append(g.h[2:dev0], s, d_, c, flags=EDGES_UNDIRECTED)
+    o.exploit()
+    t_setup = time.perf_counter() - t0
+    times = []
+    for i, (lo, hi) in enumerate(dev_batches):
+        s, d_, c = g.batch(lo, hi, directed=False)
+        t = time.perf_counter()
+        nprom = o.append(g.h[lo:hi], s, d_, c, flags=EDGES_UNDIRECTED)
+        if nprom > 0:
+            o.exploit()
+        o.best_path()
+        dt = time.perf_counter() - t
+        if i >= a.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    model, ncpu = cpu_info()
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(a), "d": a.d, "n": a.n, "S": a.S, "gamma": a.gamma,
+                   "boxes": a.boxes, "parallelism": "serial oracle"},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": 1, "kind": "oracle",
+                         "sample": f"{a.steps} timed S={a.S} steps after {a.warmup} warm-up; "
+                                   f"oracle state built by itself at n={dev0} ({t_setup:.1f}s "
+                                   f"untimed); 1 of {ncpu} cores ({model})"},
+        "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
