@@ -36,16 +36,15 @@ sys.path.insert(0, ROOT)
 METRIC = "ms per converged PI exploitation + edge relaxations/s (GTEPS) vs gather roofline"
 
 # algorithmic bytes per unit of work
-B_RELAX = 20.0      # idx i32 + cost f64 streamed (12 B) + g[u] gather (8 B)
+B_RELAX = 20.0      # Improve relaxation: idx i32 + cost f64 streamed (12 B) + g[u] gather (8 B)
 B_IVERT = 40.0      # Improve vertex: 4 row offsets (32 B) + g[v] (8 B)
-B_VISIT = 37.0      # Evaluate visit: parent 4, pc 8, g[p] 8, g write 8, h 8, b 1
-B_KIDX = 16.0       # children index per vertex per Evaluate: parent 4, count 4, rank 4, kids 4
-B_COMPACT = 1.0     # promising flag per vertex per iteration
+B_SCAN = 8.0        # Evaluate out-row entry: idx i32 (4 B) + parent[c] gather (4 B)
+B_VISIT = 38.0      # Evaluate child visit: stamp 4, pc 8, g read 8, g write 8, h 8, b 2
 
 
 def algo_bytes(st, n):
-    return (st.relaxations * B_RELAX + st.improve_set * B_IVERT + st.eval_visits * B_VISIT
-            + st.children_index * B_KIDX + st.iterations * n * B_COMPACT)
+    return (st.relaxations * B_RELAX + st.improve_set * B_IVERT + st.eval_scanned * B_SCAN
+            + st.eval_visits * B_VISIT)
 
 
 def parse():
@@ -272,7 +271,7 @@ def run_cuda(a, rank, world):
         "clocks": clk, "t_gen": t_gen, "t_pre": t_pre,
         "iters": [s.iterations for s in ex], "prom": [s.promising for s in ex],
         "improve_ms": sum(s.improve_ms for s in ex), "evaluate_ms": sum(s.evaluate_ms for s in ex),
-        "compact_ms": sum(s.compact_ms for s in ex),
+        "barriers": sum(s.barriers for s in ex),
         "improve_bytes": sum(s.relaxations * B_RELAX + s.improve_set * B_IVERT for s in ex),
         "max_level": max([s.max_level for s in ex] or [0]),
         "graph": {"n_total": g.n, "pairs": g.n_pairs, "mean_degree": g.mean_degree,
@@ -403,10 +402,11 @@ def main():
         "promising_mean": round(statistics.mean(res["prom"]), 1) if res["prom"] else 0,
         "relaxations_per_step": round(res["relax"] / a.steps),
         "max_level": res["max_level"],
-        "phase_ms": {"compact": round(res["compact_ms"], 4), "improve": round(res["improve_ms"], 4),
+        "phase_ms": {"improve": round(res["improve_ms"], 4),
                      "evaluate": round(res["evaluate_ms"], 4)},
+        "grid_barriers_per_exploit": round(res["barriers"] / max(1, res["n_exploits"]), 1),
         "roofline": {
-            "kernel": "exploit_kernel (persistent: compaction+Improve+Evaluate)",
+            "kernel": "exploit_kernel (persistent cooperative: Improve + Evaluate, all iterations)",
             "bound": "hbm",
             "achieved": round(achieved, 2),
             "peak": peak,

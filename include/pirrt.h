@@ -89,10 +89,10 @@ typedef struct {
     int32_t grid_blocks;     /* persistent grid used                                     */
     float device_ms;         /* exploit kernel time, CUDA events on the context stream   */
     float improve_ms;        /* time inside Improve phases (device %globaltimer)         */
-    float evaluate_ms;       /* time inside Evaluate phases incl. children index         */
-    float compact_ms;        /* time inside promising-set compaction phases              */
+    float evaluate_ms;       /* time inside Evaluate phases (device %globaltimer)        */
+    int32_t barriers;        /* grid-wide barriers executed                              */
     int64_t improve_set;     /* sum over Improves of |I| (vertices examined)             */
-    int64_t children_index;  /* vertices scanned by children-index rebuilds              */
+    int64_t eval_scanned;    /* out-edge entries scanned by Evaluate for children        */
 } pirrt_exploit_stats;
 
 /* Fill *cfg with the defaults listed above. */

@@ -9,6 +9,7 @@
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -93,18 +94,22 @@ struct pirrt_ctx {
     double* dcost[2] = {nullptr, nullptr}; int64_t dcost_cap[2] = {0, 0};
     int cur = 0;
     int64_t delta_edges = 0;
+    // out-edge index (rows by source, ids only): base + delta (double-buffered with `cur`)
+    long long* oboff = nullptr; int64_t oboff_cap = 0;
+    int* obidx = nullptr; int64_t obidx_cap = 0;
+    int64_t obase_edges = 0;
+    long long* odoff[2] = {nullptr, nullptr}; int64_t odoff_cap[2] = {0, 0};
+    int* odidx[2] = {nullptr, nullptr}; int64_t odidx_cap[2] = {0, 0};
+    // Evaluate stamps and the B lists (entry 0 = root)
+    unsigned* stamp = nullptr; int64_t stamp_cap = 0;
+    int* Bq[2] = {nullptr, nullptr}; int64_t Bq_cap[2] = {0, 0};
+    int Bsel = 0;
+    int Bcount = 0;
+    unsigned ev_next = 1;
     // scratch
     long long* cnt = nullptr; int64_t cnt_cap = 0;
     long long* scan_tmp = nullptr; int64_t scan_cap = 0;
-    // exploit workspace
-    int* Ilist = nullptr; int64_t Ilist_cap = 0;
-    int* kcnt = nullptr; int64_t kcnt_cap = 0;
-    int* krank = nullptr; int64_t krank_cap = 0;
-    int* koff = nullptr; int64_t koff_cap = 0;
-    int* kids = nullptr; int64_t kids_cap = 0;
-    int* front0 = nullptr; int64_t front0_cap = 0;
-    int* front1 = nullptr; int64_t front1_cap = 0;
-    long long* bsum = nullptr; int64_t bsum_cap = 0;
+    int* path = nullptr; int64_t path_cap = 0;   // best_path scratch (n + 1)
     DevCtl* ctl = nullptr;
     DevCtl* ctl_host = nullptr;   // pinned mirror
     // staging for host inputs
@@ -118,6 +123,8 @@ struct pirrt_ctx {
     unsigned char* s_b = nullptr; int64_t s_b_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool broken = false;
+    unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
+    double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
 };
 
@@ -145,15 +152,20 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
     if ((rc = grow(c->boff, c->boff_cap, cap + 1, n + 1, s))) return rc;
     if ((rc = grow(c->doff[c->cur], c->doff_cap[c->cur], cap + 1, n + 1, s))) return rc;
     if ((rc = grow(c->doff[1 - c->cur], c->doff_cap[1 - c->cur], cap + 1, 0, s))) return rc;
-    if ((rc = grow(c->cnt, c->cnt_cap, cap + 1, 0, s))) return rc;
+    if ((rc = grow(c->cnt, c->cnt_cap, 2 * (cap + 1), 0, s))) return rc;
     if ((rc = grow(c->scan_tmp, c->scan_cap, (int64_t)scan_tmp_elems(cap + 1), 0, s))) return rc;
-    if ((rc = grow(c->Ilist, c->Ilist_cap, cap, 0, s))) return rc;
-    if ((rc = grow(c->kcnt, c->kcnt_cap, cap + 1, 0, s))) return rc;
-    if ((rc = grow(c->krank, c->krank_cap, cap, 0, s))) return rc;
-    if ((rc = grow(c->koff, c->koff_cap, cap + 1, 0, s))) return rc;
-    if ((rc = grow(c->kids, c->kids_cap, cap, 0, s))) return rc;
-    if ((rc = grow(c->front0, c->front0_cap, cap, 0, s))) return rc;
-    if ((rc = grow(c->front1, c->front1_cap, cap, 0, s))) return rc;
+    if ((rc = grow(c->oboff, c->oboff_cap, cap + 1, n + 1, s))) return rc;
+    if ((rc = grow(c->odoff[c->cur], c->odoff_cap[c->cur], cap + 1, n + 1, s))) return rc;
+    if ((rc = grow(c->odoff[1 - c->cur], c->odoff_cap[1 - c->cur], cap + 1, 0, s))) return rc;
+    {
+        const int64_t old_cap = c->stamp_cap;
+        if ((rc = grow(c->stamp, c->stamp_cap, cap, n, s))) return rc;
+        if (c->stamp_cap > old_cap)   // fresh slots must read as "never visited"
+            CU(cudaMemsetAsync(c->stamp + n, 0, (size_t)(c->stamp_cap - n) * sizeof(unsigned), s));
+    }
+    if ((rc = grow(c->Bq[c->Bsel], c->Bq_cap[c->Bsel], cap + 1, 1 + c->Bcount, s))) return rc;
+    if ((rc = grow(c->Bq[1 - c->Bsel], c->Bq_cap[1 - c->Bsel], cap + 1, 1, s))) return rc;
+    if ((rc = grow(c->path, c->path_cap, cap + 2, 0, s))) return rc;
     c->vcap = cap;
     return 0;
 }
@@ -161,9 +173,9 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
 void free_all(pirrt_ctx* c) {
     void* ptrs[] = {c->g, c->h, c->pc, c->parent, c->b, c->boff, c->bidx, c->bcost,
                     c->doff[0], c->doff[1], c->didx[0], c->didx[1], c->dcost[0], c->dcost[1],
-                    c->cnt, c->scan_tmp, c->Ilist, c->kcnt, c->krank, c->koff, c->kids,
-                    c->front0, c->front1, c->bsum, c->ctl, c->s_src, c->s_dst, c->s_cost,
-                    c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b};
+                    c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
+                    c->stamp, c->Bq[0], c->Bq[1], c->path, c->cnt, c->scan_tmp, c->ctl,
+                    c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
@@ -190,38 +202,55 @@ int read_ctl(pirrt_ctx* c) {
     return 0;
 }
 
-int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
-    // fold the delta into the base when it outgrows sqrt(8 m |base|) (and 32k
-    // edges): per-append merge cost O(delta) balances amortised O(|E|)
-    // compaction cost
-    double thr = std::sqrt(8.0 * (double)std::max<int64_t>(m_dir, 1) * (double)c->base_edges);
-    thr = std::max(thr, 32768.0);
-    if ((double)c->delta_edges <= thr) return 0;
-    const int64_t E = c->base_edges + c->delta_edges;
+// fold one delta CSR into its base CSR (cost arrays NULL for the out-index)
+template <class Cost>
+int fold(pirrt_ctx* c, long long*& boff, int64_t& boff_cap, int*& bidx, int64_t& bidx_cap,
+         Cost*& bcost, int64_t& bcost_cap, long long* doff, const int* didx, const Cost* dcost,
+         int64_t E) {
     long long* nboff = nullptr; int64_t nboff_cap = 0;
     int* nbidx = nullptr; int64_t nbidx_cap = 0;
     double* nbcost = nullptr; int64_t nbcost_cap = 0;
     int rc;
     if ((rc = grow(nboff, nboff_cap, c->vcap + 1, 0, c->stream))) return rc;
     if ((rc = grow(nbidx, nbidx_cap, E + E / 4, 0, c->stream))) return rc;
-    if ((rc = grow(nbcost, nbcost_cap, E + E / 4, 0, c->stream))) return rc;
+    if (bcost && (rc = grow(nbcost, nbcost_cap, E + E / 4, 0, c->stream))) return rc;
     CompactArgs a;
-    a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
-    a.doff = c->doff[c->cur]; a.didx = c->didx[c->cur]; a.dcost = c->dcost[c->cur];
+    a.boff = boff; a.bidx = bidx; a.bcost = (const double*)bcost;
+    a.doff = doff; a.didx = didx; a.dcost = (const double*)dcost;
     a.boff_new = nboff; a.bidx_new = nbidx; a.bcost_new = nbcost;
     a.cnt = c->cnt; a.scan_tmp = c->scan_tmp; a.n = c->n;
     const long long l0 = g_kernel_launches;
     CU(launch_compact(a, c->stream));
     c->launches += g_kernel_launches - l0;
-    CU(cudaMemsetAsync(c->doff[c->cur], 0, (size_t)(c->n + 1) * sizeof(long long), c->stream));
+    CU(cudaMemsetAsync(doff, 0, (size_t)(c->n + 1) * sizeof(long long), c->stream));
     CU(cudaStreamSynchronize(c->stream));
-    if (c->boff) cudaFree(c->boff);
-    if (c->bidx) cudaFree(c->bidx);
-    if (c->bcost) cudaFree(c->bcost);
-    c->boff = nboff; c->boff_cap = nboff_cap;
-    c->bidx = nbidx; c->bidx_cap = nbidx_cap;
-    c->bcost = nbcost; c->bcost_cap = nbcost_cap;
+    cudaFree(boff); cudaFree(bidx);
+    if (bcost) cudaFree(bcost);
+    boff = nboff; boff_cap = nboff_cap;
+    bidx = nbidx; bidx_cap = nbidx_cap;
+    bcost = (Cost*)nbcost; bcost_cap = nbcost_cap;
+    return 0;
+}
+
+int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
+    // fold the deltas into the bases when they outgrow sqrt(8 m |base|) (and
+    // 32k edges): the per-append merge cost O(delta) balances the amortised
+    // O(|E|) fold
+    double thr = std::sqrt(8.0 * (double)std::max<int64_t>(m_dir, 1) * (double)c->base_edges);
+    thr = std::max(thr, c->compact_min);
+    if ((double)c->delta_edges <= thr) return 0;
+    const int64_t E = c->base_edges + c->delta_edges;
+    int rc;
+    if ((rc = fold<double>(c, c->boff, c->boff_cap, c->bidx, c->bidx_cap, c->bcost, c->bcost_cap,
+                           c->doff[c->cur], c->didx[c->cur], c->dcost[c->cur], E)))
+        return rc;
+    double* no_cost = nullptr;
+    int64_t no_cap = 0;
+    if ((rc = fold<double>(c, c->oboff, c->oboff_cap, c->obidx, c->obidx_cap, no_cost, no_cap,
+                           c->odoff[c->cur], c->odidx[c->cur], nullptr, E)))
+        return rc;
     c->base_edges = E;
+    c->obase_edges = E;
     c->delta_edges = 0;
     return 0;
 }
@@ -251,6 +280,9 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     CU(cudaSetDevice(cfg.device));
     pirrt_ctx* c = new pirrt_ctx();
     c->cfg = cfg;
+    if (const char* w = std::getenv("PIRRT_WATCHDOG_MS"))
+        c->watchdog_ns = (unsigned long long)std::strtoull(w, nullptr, 10) * 1000000ull;
+    if (const char* w = std::getenv("PIRRT_COMPACT_MIN")) c->compact_min = std::atof(w);
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -278,7 +310,9 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     }
     if ((rc = grow(c->bidx, c->bidx_cap, 64, 0, c->stream))) return bail(rc);
     if ((rc = grow(c->bcost, c->bcost_cap, 64, 0, c->stream))) return bail(rc);
-    if ((rc = grow(c->bsum, c->bsum_cap, c->grid_blocks + 1, 0, c->stream))) return bail(rc);
+    if ((rc = grow(c->obidx, c->obidx_cap, 64, 0, c->stream))) return bail(rc);
+    for (int k = 0; k < 2; ++k)
+        if ((rc = grow(c->odidx[k], c->odidx_cap[k], ecap0, 0, c->stream))) return bail(rc);
     if (cudaMalloc(&c->ctl, sizeof(DevCtl)) != cudaSuccess) return bail(fail(PIRRT_E_NOMEM, "ctl"));
     if (cudaMallocHost(&c->ctl_host, sizeof(DevCtl)) != cudaSuccess)
         return bail(fail(PIRRT_E_NOMEM, "ctl host"));
@@ -296,6 +330,10 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         cudaMemsetAsync(c->b, 0, 2, s) != cudaSuccess ||
         cudaMemsetAsync(c->boff, 0, 3 * sizeof(long long), s) != cudaSuccess ||
         cudaMemsetAsync(c->doff[0], 0, 3 * sizeof(long long), s) != cudaSuccess ||
+        cudaMemsetAsync(c->oboff, 0, 3 * sizeof(long long), s) != cudaSuccess ||
+        cudaMemsetAsync(c->odoff[0], 0, 3 * sizeof(long long), s) != cudaSuccess ||
+        cudaMemsetAsync(c->Bq[0], 0, sizeof(int), s) != cudaSuccess ||   // Bq[k][0] = root = 0
+        cudaMemsetAsync(c->Bq[1], 0, sizeof(int), s) != cudaSuccess ||
         cudaMemsetAsync(c->ctl, 0, sizeof(DevCtl), s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "create: init copies"));
@@ -341,6 +379,7 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     const int64_t dneed = c->delta_edges + m_dir;
     if ((rc = grow(c->didx[nb], c->didx_cap[nb], dneed, 0, s))) return rc;
     if ((rc = grow(c->dcost[nb], c->dcost_cap[nb], dneed, 0, s))) return rc;
+    if ((rc = grow(c->odidx[nb], c->odidx_cap[nb], dneed, 0, s))) return rc;
     // inputs
     const double *d_h = nullptr, *d_g = nullptr, *d_cost = nullptr;
     const int *d_parent = nullptr, *d_src = nullptr, *d_dst = nullptr;
@@ -357,6 +396,12 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     a.doff_old = c->doff[c->cur]; a.didx_old = c->didx[c->cur]; a.dcost_old = c->dcost[c->cur];
     a.doff_new = c->doff[nb]; a.didx_new = c->didx[nb]; a.dcost_new = c->dcost[nb];
     a.boff_w = c->boff;
+    a.oboff = c->oboff; a.obidx = c->obidx;
+    a.odoff_old = c->odoff[c->cur]; a.odidx_old = c->odidx[c->cur];
+    a.odoff_new = c->odoff[nb]; a.odidx_new = c->odidx[nb];
+    a.oboff_w = c->oboff;
+    a.obase_edges = c->obase_edges;
+    a.Blist = c->Bq[c->Bsel]; a.Bcount = c->Bcount;
     a.cnt = c->cnt; a.scan_tmp = c->scan_tmp;
     a.h_in = d_h; a.parent_in = parent_new ? d_parent : nullptr; a.g_in = g_new ? d_g : nullptr;
     a.src = d_src; a.dst = d_dst; a.cost = d_cost; a.m = n_edges;
@@ -380,6 +425,7 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     c->cur = nb;
     c->n = n_all;
     c->delta_edges += m_dir;
+    c->Bcount += c->ctl_host->nprom;
     if (n_new_promising) *n_new_promising = c->ctl_host->nprom;
     if ((rc = compact_if_needed(c, m_dir))) { c->broken = true; return rc; }
     return PIRRT_OK;
@@ -394,14 +440,18 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     ExploitArgs a;
     a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
     a.doff = c->doff[c->cur]; a.didx = c->didx[c->cur]; a.dcost = c->dcost[c->cur];
+    a.oboff = c->oboff; a.obidx = c->obidx;
+    a.odoff = c->odoff[c->cur]; a.odidx = c->odidx[c->cur];
     a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
-    a.Ilist = c->Ilist; a.kcnt = c->kcnt; a.krank = c->krank; a.koff = c->koff; a.kids = c->kids;
-    a.front0 = c->front0; a.front1 = c->front1; a.bsum = c->bsum;
+    a.stamp = c->stamp;
+    a.Bq0 = c->Bq[0]; a.Bq1 = c->Bq[1]; a.Bsel = c->Bsel; a.Bcount = c->Bcount;
+    a.ev_base = c->ev_next;
     a.ctl = c->ctl;
     a.n = c->n;
     a.max_it = c->cfg.max_iterations;
     a.eps = c->cfg.epsilon;
     a.prune_off = (c->cfg.flags & PIRRT_F_PRUNE_OFF) ? 1 : 0;
+    a.watchdog_ns = c->watchdog_ns;
     CU(cudaEventRecord(c->ev0, s));
     const long long l0 = g_kernel_launches;
     cudaError_t e = launch_exploit(a, c->grid_blocks, s);
@@ -410,6 +460,9 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     CU(cudaEventRecord(c->ev1, s));
     if ((rc = read_ctl(c))) { c->broken = true; return rc; }
     const DevCtl& h = *c->ctl_host;
+    c->Bsel = h.Bsel_out;
+    c->Bcount = h.Bcount_out;
+    c->ev_next += (unsigned)h.evaluations;
     if (st) {
         std::memset(st, 0, sizeof(*st));
         st->iterations = h.iterations;
@@ -426,9 +479,14 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
         st->device_ms = ms;
         st->improve_ms = (float)(h.t_improve * 1e-6);
         st->evaluate_ms = (float)(h.t_evaluate * 1e-6);
-        st->compact_ms = (float)(h.t_compact * 1e-6);
+
         st->improve_set = h.improve_set;
-        st->children_index = h.children_index;
+        st->eval_scanned = h.eval_scanned;
+        st->barriers = h.barriers;
+    }
+    if (h.abort_at) {
+        c->broken = true;
+        return fail(PIRRT_E_STATE, "exploit: watchdog fired (PIRRT_WATCHDOG_MS); context unusable");
     }
     if (h.status == PIRRT_E_NOCONV) return fail(PIRRT_E_NOCONV, "exploit: iteration cap exceeded");
     return PIRRT_OK;
@@ -465,13 +523,14 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     int rc;
     if ((rc = set_device(c))) return rc;
     cudaStream_t s = c->stream;
-    // path_rev lives in front1 (workspace, n entries), its length in kcnt[n]
+    // path_rev in path[0..n], its length in path[path_cap - 1]
+    int* len_dev = c->path + (c->path_cap - 1);
     const long long l0 = g_kernel_launches;
-    CU(launch_best_path(c->parent, c->n, c->front1, c->kcnt + c->n, s));
+    CU(launch_best_path(c->parent, c->n, c->path, len_dev, s));
     c->launches += g_kernel_launches - l0;
     int len = 0;
     double gg = 0.0;
-    CU(cudaMemcpyAsync(&len, c->kcnt + c->n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&len, len_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(&gg, c->g + kGoal, sizeof(double), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     if (std::isinf(gg)) {
@@ -481,7 +540,7 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     }
     if (len < 0) return fail(PIRRT_E_CORRUPT, "best_path: parent cycle");
     std::vector<int> rev(len);
-    CU(cudaMemcpyAsync(rev.data(), c->front1, (size_t)len * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(rev.data(), c->path, (size_t)len * sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     if (len == 0 || rev.back() != kRoot)
         return fail(PIRRT_E_CORRUPT, "best_path: goal branch does not reach the root");
@@ -540,8 +599,29 @@ int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, con
     } else {
         CU(cudaMemsetAsync(c->b, 0, (size_t)n, s));
     }
+    // the B list is the device-side representation of b
+    int* cnt_dev = c->path + (c->path_cap - 1);
+    const long long l1 = g_kernel_launches;
+    CU(launch_rebuild_blist(c->b, n, c->Bq[c->Bsel], cnt_dev, c->cnt, c->scan_tmp, s));
+    c->launches += g_kernel_launches - l1;
+    int bc = 0;
+    CU(cudaMemcpyAsync(&bc, cnt_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    c->Bcount = bc;
     return PIRRT_OK;
 }
 
 }  // extern "C"
+
+// ---- debug-only export (not part of include/pirrt.h): the device B list
+extern "C" int pirrt_debug_blist(const pirrt_ctx* c, int32_t* out, int64_t cap, int32_t* count) {
+    if (!c || !out || !count) return fail(PIRRT_E_INVAL, "debug_blist: NULL");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    *count = c->Bcount;
+    if (cap < c->Bcount + 1) return fail(PIRRT_E_RANGE, "debug_blist: capacity");
+    CU(cudaMemcpyAsync(out, c->Bq[c->Bsel], (size_t)(c->Bcount + 1) * sizeof(int),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return PIRRT_OK;
+}

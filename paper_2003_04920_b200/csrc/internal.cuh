@@ -26,26 +26,28 @@ struct IterCtl {
     unsigned long long dg_bits;   // atomicMax of Delta g (non-negative f64 bits)
     long long relax;              // relaxations this Improve
     long long visits;             // children visited this Evaluate
-    int I_count;                  // |I|
-    int oldB;                     // |B| before Evaluate
+    long long scanned;            // out-row entries scanned this Evaluate
+    int tasks;                    // |I|
     int ptr_changed;              // some parent value changed in Improve
     int g_changed;                // some g bit changed in Evaluate
-    int newB;                     // |B| after Evaluate
     int both;                     // |old B  n  new B|
-    int pad[2];
+    int lpush[3];                 // expanded vertices per BFS level (rotating slots)
+    int lvis[3];                  // "some child visited" per BFS level (rotating slots)
 };
 
 // Device control block (one per context, cudaMalloc'ed, 8-byte aligned).
+// Everything up to `err` is zeroed before each exploit.
 struct DevCtl {
     IterCtl it[2];
-    int fcount[3];                // frontier sizes (3-rotation over levels)
-    int vcount[3];                // "visited at this level" flags
     // exploit outputs
     int status;                   // 0 ok, PIRRT_E_NOCONV
     int iterations, evaluations, max_level, promising, stalled;
+    int Bsel_out, Bcount_out;     // B list after the exploit
+    int barriers;
+    int abort_at;                 // watchdog: barrier index at which all threads stop
     double last_dg;
-    long long relaxations, eval_visits, improve_set, children_index;
-    unsigned long long t_compact, t_improve, t_evaluate;
+    long long relaxations, eval_visits, improve_set, eval_scanned;
+    unsigned long long t_improve, t_evaluate;
     // append / set_policy
     int err;                      // bitmask of kErr*
     int nprom;                    // new promising vertices
@@ -56,33 +58,37 @@ struct DevCtl {
 
 // Everything the persistent exploit kernel touches.
 struct ExploitArgs {
-    // in-edge store: base CSR + delta CSR, rows by destination vertex
+    // in-edge store (rows by destination): base CSR + delta CSR -- Improve
     const long long* __restrict__ boff;
     const int* __restrict__ bidx;
     const double* __restrict__ bcost;
     const long long* __restrict__ doff;
     const int* __restrict__ didx;
     const double* __restrict__ dcost;
+    // out-edge index (rows by source, ids only): base + delta -- Evaluate
+    const long long* __restrict__ oboff;
+    const int* __restrict__ obidx;
+    const long long* __restrict__ odoff;
+    const int* __restrict__ odidx;
     // vertex SoA + policy-edge cost pc (R9)
     double* g;
     const double* h;
     int* parent;
     double* pc;
     unsigned char* b;
-    // workspace
-    int* Ilist;                   // [n] improve set
-    int* kcnt;                    // [n+1] children counts
-    int* krank;                   // [n] rank of v among its parent's children
-    int* koff;                    // [n+1] children offsets
-    int* kids;                    // [n] children index
-    int* front0;                  // [n] BFS frontier buffers
-    int* front1;
-    long long* bsum;              // [grid] block partial sums
+    unsigned* stamp;              // 2e: visited in Evaluate e; 2e+1: expanded in e
+    // B lists (entry 0 = root, B = [1, 1 + count)); Bq[Bsel] is current
+    int* Bq0;
+    int* Bq1;
+    int Bsel;
+    int Bcount;
+    unsigned ev_base;             // id of this exploit's first Evaluate
     DevCtl* ctl;
     int n;
     int max_it;
     double eps;
     int prune_off;
+    unsigned long long watchdog_ns;   // abort the loop after this long (diagnostic guard)
 };
 
 // kernels launched by this host thread (diagnostics; abi.cu attributes the
@@ -99,6 +105,11 @@ struct AppendArgs {
     const long long* doff_old; const int* didx_old; const double* dcost_old;
     // new delta (write)
     long long* doff_new; int* didx_new; double* dcost_new;
+    // out-edge index: committed base/delta (read) and new delta (write)
+    const long long* oboff; const int* obidx;
+    const long long* odoff_old; const int* odidx_old;
+    long long* odoff_new; int* odidx_new;
+    long long* oboff_w;
     long long* boff_w;            // writable base offsets (rows n_old+1..n_all filled)
     long long* cnt;               // [n_all+1] scratch counts / cursors
     long long* scan_tmp;          // scan partials
@@ -112,11 +123,15 @@ struct AppendArgs {
     double* g; double* h; int* parent; double* pc; unsigned char* b;
     int n_old, n_new;
     long long base_edges;
+    long long obase_edges;
+    int* Blist;                   // current B list; new promising vertices go to [1+Bcount+k]
+    int Bcount;
     DevCtl* ctl;
     int grid_blocks;
 };
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t s);
 
+// fold a delta CSR into its base CSR (cost arrays may be NULL: out-index)
 struct CompactArgs {
     const long long* boff; const int* bidx; const double* bcost;
     const long long* doff; const int* didx; const double* dcost;
@@ -134,6 +149,10 @@ struct PolicyArgs {
     int n; DevCtl* ctl;
 };
 cudaError_t launch_set_policy(const PolicyArgs& a, cudaStream_t s);
+
+// B list = {v : b[v] == 1} in ascending order into list[1..]; count -> *count_out
+cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* count_out,
+                                 long long* cnt, long long* scan_tmp, cudaStream_t s);
 
 cudaError_t launch_best_path(const int* parent, int n, int* path_rev, int* len_out,
                              cudaStream_t s);

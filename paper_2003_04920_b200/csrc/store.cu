@@ -158,13 +158,17 @@ __global__ void k_delta_count(const long long* doff_old, int n_old, int n_all, l
         cnt[v] = (v < n_old) ? doff_old[v + 1] - doff_old[v] : 0;
 }
 
-__global__ void k_edge_hist(const int* src, const int* dst, long long m, int undirected,
+// dir 0: in-edge store (row = dst, value = src, with cost);
+// dir 1: out-edge index (row = src, value = dst, no cost).
+// With `undirected` every triple also contributes the reverse edge.
+__global__ void k_edge_hist(const int* src, const int* dst, long long m, int undirected, int dir,
                             long long* cnt, const DevCtl* ctl) {
     if (failed(ctl)) return;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        atomicAdd((unsigned long long*)&cnt[dst[e]], 1ull);
-        if (undirected) atomicAdd((unsigned long long*)&cnt[src[e]], 1ull);
+        const int row = dir ? src[e] : dst[e];
+        atomicAdd((unsigned long long*)&cnt[row], 1ull);
+        if (undirected) atomicAdd((unsigned long long*)&cnt[dir ? dst[e] : src[e]], 1ull);
     }
 }
 
@@ -186,7 +190,7 @@ __global__ void k_delta_copy_old(const long long* doff_old, const int* didx_old,
             len = s1 - s0;
             for (long long k = lane; k < len; k += 32) {
                 didx_new[dst0 + k] = didx_old[s0 + k];
-                dcost_new[dst0 + k] = dcost_old[s0 + k];
+                if (dcost_new) dcost_new[dst0 + k] = dcost_old[s0 + k];
             }
         }
         if (lane == 0) cursor[v] = dst0 + len;
@@ -194,20 +198,21 @@ __global__ void k_delta_copy_old(const long long* doff_old, const int* didx_old,
 }
 
 __global__ void k_delta_scatter(const int* src, const int* dst, const double* cost, long long m,
-                                int undirected, long long* cursor, int* didx_new,
+                                int undirected, int dir, long long* cursor, int* didx_new,
                                 double* dcost_new, const DevCtl* ctl) {
     if (failed(ctl)) return;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         const int s = src[e], d = dst[e];
-        const double c = cost[e] + 0.0;   // -0.0 -> +0.0 (R12)
-        long long p = (long long)atomicAdd((unsigned long long*)&cursor[d], 1ull);
-        didx_new[p] = s;
-        dcost_new[p] = c;
+        const int row = dir ? s : d, val = dir ? d : s;
+        long long p = (long long)atomicAdd((unsigned long long*)&cursor[row], 1ull);
+        didx_new[p] = val;
+        const double c = dcost_new ? cost[e] + 0.0 : 0.0;   // -0.0 -> +0.0 (R12)
+        if (dcost_new) dcost_new[p] = c;
         if (undirected) {
-            p = (long long)atomicAdd((unsigned long long*)&cursor[s], 1ull);
-            didx_new[p] = d;
-            dcost_new[p] = c;
+            p = (long long)atomicAdd((unsigned long long*)&cursor[val], 1ull);
+            didx_new[p] = row;
+            if (dcost_new) dcost_new[p] = c;
         }
     }
 }
@@ -344,20 +349,46 @@ __global__ void __launch_bounds__(kBT) k_relax_new(
     }
 }
 
-// b(v) = g(v) + h(v) < g(x_goal) for the new vertices
+// b(v) = g(v) + h(v) < g(x_goal) for the new vertices;
+// promising ones are appended to the B list (invisible until the host
+// commits the new count)
 __global__ void k_new_promising(const double* g, const double* h, unsigned char* b, int n_old,
-                                int n_new, DevCtl* ctl) {
+                                int n_new, int* Blist, int Bcount, DevCtl* ctl) {
     if (failed(ctl)) return;
     const double thr = g[kGoal];
-    int cnt = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int base = blockIdx.x * blockDim.x; base < n_new; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
         const int v = n_old + i;
-        const unsigned char p = (g[v] + h[v] < thr) ? 1 : 0;
-        b[v] = p;
-        cnt += p;
+        const bool p = (i < n_new) && (g[v] + h[v] < thr);
+        if (i < n_new) b[v] = p ? 1 : 0;
+        const unsigned m = __ballot_sync(kFull, p);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            int pos = 0;
+            if (lane == leader) pos = atomicAdd(&ctl->nprom, __popc(m));
+            pos = __shfl_sync(kFull, pos, leader);
+            unsigned lt;
+            asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
+            if (p) Blist[1 + Bcount + pos + __popc(m & lt)] = v;
+        }
     }
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctl->nprom, cnt);
+}
+
+// B list rebuild (set_policy): flags then scan then scatter in id order
+__global__ void k_b_flags(const unsigned char* b, int n, long long* cnt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        cnt[v] = (v != kRoot && b[v] == 1) ? 1 : 0;
+}
+
+__global__ void k_b_scatter(const unsigned char* b, int n, const long long* off, int* list,
+                            int* count_out) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        if (v != kRoot && b[v] == 1) list[1 + off[v]] = v;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        list[0] = kRoot;
+        *count_out = (int)off[n];
+    }
 }
 
 // ------------------------------------------------------------------ compaction
@@ -377,13 +408,13 @@ __global__ void k_base_merge(const long long* boff, const int* bidx, const doubl
         const long long b0 = boff[v], bl = boff[v + 1] - b0;
         for (long long k = lane; k < bl; k += 32) {
             bidx_new[o + k] = bidx[b0 + k];
-            bcost_new[o + k] = bcost[b0 + k];
+            if (bcost_new) bcost_new[o + k] = bcost[b0 + k];
         }
         o += bl;
         const long long d0 = doff[v], dl = doff[v + 1] - d0;
         for (long long k = lane; k < dl; k += 32) {
             bidx_new[o + k] = didx[d0 + k];
-            bcost_new[o + k] = dcost[d0 + k];
+            if (bcost_new) bcost_new[o + k] = dcost[d0 + k];
         }
     }
 }
@@ -447,26 +478,36 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
         k_validate<<<grid_for(work), kBT, 0, s>>>(a.src, a.dst, a.cost, m, a.h_in, a.parent_in,
                                                   a.g_in, a.n_old, a.n_new, a.ctl);
     }
-    // 2. delta merge (counting sort of the new edges by destination)
-    ++g_kernel_launches;
-    k_delta_count<<<grid_for(n_all + 1), kBT, 0, s>>>(a.doff_old, a.n_old, n_all, a.cnt, a.ctl);
-    if (m > 0) {
+    // 2. delta merge (counting sort of the new edges by row), in-edge store
+    //    (rows by destination, with cost) and out-edge index (rows by source)
+    for (int dir = 0; dir < 2; ++dir) {
+        const long long* doff_old = dir ? a.odoff_old : a.doff_old;
+        const int* didx_old = dir ? a.odidx_old : a.didx_old;
+        const double* dcost_old = dir ? nullptr : a.dcost_old;
+        long long* doff_new = dir ? a.odoff_new : a.doff_new;
+        int* didx_new = dir ? a.odidx_new : a.didx_new;
+        double* dcost_new = dir ? nullptr : a.dcost_new;
         ++g_kernel_launches;
-        k_edge_hist<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, m, a.undirected, a.cnt, a.ctl);
-    }
-    if ((e = scan_exclusive(a.cnt, a.doff_new, n_all, a.scan_tmp, s)) != cudaSuccess) return e;
-    ++g_kernel_launches;
-    k_delta_copy_old<<<grid_for((long long)n_all * 32), kBT, 0, s>>>(
-        a.doff_old, a.didx_old, a.dcost_old, a.doff_new, a.didx_new, a.dcost_new, a.n_old, n_all,
-        a.cnt, a.ctl);
-    if (m > 0) {
+        k_delta_count<<<grid_for(n_all + 1), kBT, 0, s>>>(doff_old, a.n_old, n_all, a.cnt, a.ctl);
+        if (m > 0) {
+            ++g_kernel_launches;
+            k_edge_hist<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, m, a.undirected, dir, a.cnt, a.ctl);
+        }
+        if ((e = scan_exclusive(a.cnt, doff_new, n_all, a.scan_tmp, s)) != cudaSuccess) return e;
         ++g_kernel_launches;
-        k_delta_scatter<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, a.cost, m, a.undirected, a.cnt,
-                                                    a.didx_new, a.dcost_new, a.ctl);
+        k_delta_copy_old<<<grid_for((long long)n_all * 32), kBT, 0, s>>>(
+            doff_old, didx_old, dcost_old, doff_new, didx_new, dcost_new, a.n_old, n_all, a.cnt,
+            a.ctl);
+        if (m > 0) {
+            ++g_kernel_launches;
+            k_delta_scatter<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, a.cost, m, a.undirected, dir,
+                                                        a.cnt, didx_new, dcost_new, a.ctl);
+        }
+        ++g_kernel_launches;
+        k_base_extend<<<grid_for(a.n_new + 1), kBT, 0, s>>>(dir ? a.oboff_w : a.boff_w, a.n_old,
+                                                            n_all, dir ? a.obase_edges : a.base_edges,
+                                                            a.ctl);
     }
-    ++g_kernel_launches;
-    k_base_extend<<<grid_for(a.n_new + 1), kBT, 0, s>>>(a.boff_w, a.n_old, n_all, a.base_edges,
-                                                        a.ctl);
     // 3. new vertex state
     if (a.n_new > 0) {
         ++g_kernel_launches;
@@ -503,7 +544,8 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
                 return e;
         }
         ++g_kernel_launches;
-        k_new_promising<<<grid_for(a.n_new), kBT, 0, s>>>(a.g, a.h, a.b, a.n_old, a.n_new, a.ctl);
+        k_new_promising<<<grid_for(a.n_new), kBT, 0, s>>>(a.g, a.h, a.b, a.n_old, a.n_new, a.Blist,
+                                                          a.Bcount, a.ctl);
     }
     return cudaGetLastError();
 }
@@ -527,6 +569,17 @@ cudaError_t launch_set_policy(const PolicyArgs& a, cudaStream_t s) {
     k_find_pc<<<grid_for((long long)a.n * 32), kBT, 0, s>>>(a.boff, a.bidx, a.bcost, a.doff, a.didx,
                                                             a.dcost, a.parent_in, a.g_in, a.pc, 0,
                                                             a.n, 0, a.ctl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* count_out,
+                                 long long* cnt, long long* scan_tmp, cudaStream_t s) {
+    cudaError_t e;
+    ++g_kernel_launches;
+    k_b_flags<<<grid_for(n), kBT, 0, s>>>(b, n, cnt);
+    if ((e = scan_exclusive(cnt, cnt + n + 1, n, scan_tmp, s)) != cudaSuccess) return e;
+    ++g_kernel_launches;
+    k_b_scatter<<<grid_for(n), kBT, 0, s>>>(b, n, cnt + n + 1, list, count_out);
     return cudaGetLastError();
 }
 

@@ -77,9 +77,9 @@ class pirrt_exploit_stats(C.Structure):
         ("device_ms", C.c_float),
         ("improve_ms", C.c_float),
         ("evaluate_ms", C.c_float),
-        ("compact_ms", C.c_float),
+        ("barriers", C.c_int32),
         ("improve_set", C.c_int64),
-        ("children_index", C.c_int64),
+        ("eval_scanned", C.c_int64),
     ]
 
 
@@ -156,9 +156,9 @@ class ExploitStats:
     device_ms: float
     improve_ms: float
     evaluate_ms: float
-    compact_ms: float
+    barriers: int
     improve_set: int
-    children_index: int
+    eval_scanned: int
 
 
 def _is_torch_cuda(a) -> bool:
