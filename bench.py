@@ -238,6 +238,10 @@ def run_cuda(a, rank, world):
     torch.cuda.nvtx.range_pop()
     launches = ctx.kernel_launches - l0
     step_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(a.warmup, a.warmup + a.steps)]
+    if os.environ.get("PIRRT_BENCH_VERBOSE"):
+        for i, (ms, st) in enumerate(zip(step_ms, stats)):
+            print(f"dev step {i}: {ms:.3f} ms exploit={st.device_ms if st else 0:.3f} "
+                  f"it={st.iterations if st else 0}", file=sys.stderr, flush=True)
     total_ms = float(sum(step_ms))
     # ---- e2e leg: same ABI from pinned host buffers
     host_in = []
@@ -255,6 +259,9 @@ def run_cuda(a, rank, world):
         st, nprom, path = step(host_in[i])
         e1.record(stream)
         torch.cuda.synchronize()
+        if os.environ.get("PIRRT_BENCH_VERBOSE"):
+            print(f"e2e step {i}: {e0.elapsed_time(e1):.3f} ms edges={ctx.n_edges} "
+                  f"exploit={st.device_ms if st else 0:.3f}", file=sys.stderr, flush=True)
         if i >= a.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
             h2d += sum(x.nbytes for x in host_in[i])

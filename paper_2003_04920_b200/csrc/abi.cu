@@ -87,6 +87,11 @@ struct pirrt_ctx {
     long long* boff = nullptr; int64_t boff_cap = 0;
     int* bidx = nullptr; int64_t bidx_cap = 0;
     double* bcost = nullptr; int64_t bcost_cap = 0;
+    // spare base buffers: a fold writes the merged CSR here and swaps, so a
+    // steady-state fold allocates and frees nothing
+    long long* sboff = nullptr; int64_t sboff_cap = 0;
+    int* sbidx = nullptr; int64_t sbidx_cap = 0;
+    double* sbcost = nullptr; int64_t sbcost_cap = 0;
     int64_t base_edges = 0;
     // delta CSR, double-buffered (cur = committed)
     long long* doff[2] = {nullptr, nullptr}; int64_t doff_cap[2] = {0, 0};
@@ -97,6 +102,8 @@ struct pirrt_ctx {
     // out-edge index (rows by source, ids only): base + delta (double-buffered with `cur`)
     long long* oboff = nullptr; int64_t oboff_cap = 0;
     int* obidx = nullptr; int64_t obidx_cap = 0;
+    long long* soboff = nullptr; int64_t soboff_cap = 0;
+    int* sobidx = nullptr; int64_t sobidx_cap = 0;
     int64_t obase_edges = 0;
     long long* odoff[2] = {nullptr, nullptr}; int64_t odoff_cap[2] = {0, 0};
     int* odidx[2] = {nullptr, nullptr}; int64_t odidx_cap[2] = {0, 0};
@@ -150,11 +157,13 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
     if ((rc = grow(c->parent, c->parent_cap, cap, n, s))) return rc;
     if ((rc = grow(c->b, c->b_cap, cap, n, s))) return rc;
     if ((rc = grow(c->boff, c->boff_cap, cap + 1, n + 1, s))) return rc;
+    if ((rc = grow(c->sboff, c->sboff_cap, cap + 1, 0, s))) return rc;
     if ((rc = grow(c->doff[c->cur], c->doff_cap[c->cur], cap + 1, n + 1, s))) return rc;
     if ((rc = grow(c->doff[1 - c->cur], c->doff_cap[1 - c->cur], cap + 1, 0, s))) return rc;
     if ((rc = grow(c->cnt, c->cnt_cap, 2 * (cap + 1), 0, s))) return rc;
     if ((rc = grow(c->scan_tmp, c->scan_cap, (int64_t)scan_tmp_elems(cap + 1), 0, s))) return rc;
     if ((rc = grow(c->oboff, c->oboff_cap, cap + 1, n + 1, s))) return rc;
+    if ((rc = grow(c->soboff, c->soboff_cap, cap + 1, 0, s))) return rc;
     if ((rc = grow(c->odoff[c->cur], c->odoff_cap[c->cur], cap + 1, n + 1, s))) return rc;
     if ((rc = grow(c->odoff[1 - c->cur], c->odoff_cap[1 - c->cur], cap + 1, 0, s))) return rc;
     {
@@ -172,6 +181,7 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
 
 void free_all(pirrt_ctx* c) {
     void* ptrs[] = {c->g, c->h, c->pc, c->parent, c->b, c->boff, c->bidx, c->bcost,
+                    c->sboff, c->sbidx, c->sbcost, c->soboff, c->sobidx,
                     c->doff[0], c->doff[1], c->didx[0], c->didx[1], c->dcost[0], c->dcost[1],
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
                     c->stamp, c->Bq[0], c->Bq[1], c->path, c->cnt, c->scan_tmp, c->ctl,
@@ -202,33 +212,28 @@ int read_ctl(pirrt_ctx* c) {
     return 0;
 }
 
-// fold one delta CSR into its base CSR (cost arrays NULL for the out-index)
-template <class Cost>
+// fold one delta CSR into its base CSR: merge into the spare base buffers,
+// clear the delta, swap current and spare (cost arrays NULL for the out-index)
 int fold(pirrt_ctx* c, long long*& boff, int64_t& boff_cap, int*& bidx, int64_t& bidx_cap,
-         Cost*& bcost, int64_t& bcost_cap, long long* doff, const int* didx, const Cost* dcost,
-         int64_t E) {
-    long long* nboff = nullptr; int64_t nboff_cap = 0;
-    int* nbidx = nullptr; int64_t nbidx_cap = 0;
-    double* nbcost = nullptr; int64_t nbcost_cap = 0;
+         double*& bcost, int64_t& bcost_cap, long long*& sboff, int64_t& sboff_cap, int*& sbidx,
+         int64_t& sbidx_cap, double*& sbcost, int64_t& sbcost_cap, long long* doff,
+         const int* didx, const double* dcost, int64_t E) {
     int rc;
-    if ((rc = grow(nboff, nboff_cap, c->vcap + 1, 0, c->stream))) return rc;
-    if ((rc = grow(nbidx, nbidx_cap, E + E / 4, 0, c->stream))) return rc;
-    if (bcost && (rc = grow(nbcost, nbcost_cap, E + E / 4, 0, c->stream))) return rc;
+    if ((rc = grow(sboff, sboff_cap, c->vcap + 1, 0, c->stream))) return rc;
+    if ((rc = grow(sbidx, sbidx_cap, E, 0, c->stream))) return rc;
+    if (bcost && (rc = grow(sbcost, sbcost_cap, E, 0, c->stream))) return rc;
     CompactArgs a;
-    a.boff = boff; a.bidx = bidx; a.bcost = (const double*)bcost;
-    a.doff = doff; a.didx = didx; a.dcost = (const double*)dcost;
-    a.boff_new = nboff; a.bidx_new = nbidx; a.bcost_new = nbcost;
+    a.boff = boff; a.bidx = bidx; a.bcost = bcost;
+    a.doff = doff; a.didx = didx; a.dcost = dcost;
+    a.boff_new = sboff; a.bidx_new = sbidx; a.bcost_new = bcost ? sbcost : nullptr;
     a.cnt = c->cnt; a.scan_tmp = c->scan_tmp; a.n = c->n;
     const long long l0 = g_kernel_launches;
     CU(launch_compact(a, c->stream));
     c->launches += g_kernel_launches - l0;
     CU(cudaMemsetAsync(doff, 0, (size_t)(c->n + 1) * sizeof(long long), c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    cudaFree(boff); cudaFree(bidx);
-    if (bcost) cudaFree(bcost);
-    boff = nboff; boff_cap = nboff_cap;
-    bidx = nbidx; bidx_cap = nbidx_cap;
-    bcost = (Cost*)nbcost; bcost_cap = nbcost_cap;
+    std::swap(boff, sboff); std::swap(boff_cap, sboff_cap);
+    std::swap(bidx, sbidx); std::swap(bidx_cap, sbidx_cap);
+    if (bcost) { std::swap(bcost, sbcost); std::swap(bcost_cap, sbcost_cap); }
     return 0;
 }
 
@@ -241,13 +246,16 @@ int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
     if ((double)c->delta_edges <= thr) return 0;
     const int64_t E = c->base_edges + c->delta_edges;
     int rc;
-    if ((rc = fold<double>(c, c->boff, c->boff_cap, c->bidx, c->bidx_cap, c->bcost, c->bcost_cap,
-                           c->doff[c->cur], c->didx[c->cur], c->dcost[c->cur], E)))
+    if ((rc = fold(c, c->boff, c->boff_cap, c->bidx, c->bidx_cap, c->bcost, c->bcost_cap,
+                   c->sboff, c->sboff_cap, c->sbidx, c->sbidx_cap, c->sbcost, c->sbcost_cap,
+                   c->doff[c->cur], c->didx[c->cur], c->dcost[c->cur], E)))
         return rc;
     double* no_cost = nullptr;
-    int64_t no_cap = 0;
-    if ((rc = fold<double>(c, c->oboff, c->oboff_cap, c->obidx, c->obidx_cap, no_cost, no_cap,
-                           c->odoff[c->cur], c->odidx[c->cur], nullptr, E)))
+    double* no_scost = nullptr;
+    int64_t no_cap = 0, no_scap = 0;
+    if ((rc = fold(c, c->oboff, c->oboff_cap, c->obidx, c->obidx_cap, no_cost, no_cap,
+                   c->soboff, c->soboff_cap, c->sobidx, c->sobidx_cap, no_scost, no_scap,
+                   c->odoff[c->cur], c->odidx[c->cur], nullptr, E)))
         return rc;
     c->base_edges = E;
     c->obase_edges = E;
