@@ -110,6 +110,7 @@ struct pirrt_ctx {
     // Evaluate stamps and the B lists (entry 0 = root)
     unsigned* stamp = nullptr; int64_t stamp_cap = 0;
     int* Bq[2] = {nullptr, nullptr}; int64_t Bq_cap[2] = {0, 0};
+    int* qdepth = nullptr; int64_t qdepth_cap = 0;
     int Bsel = 0;
     int Bcount = 0;
     unsigned ev_next = 1;
@@ -132,6 +133,7 @@ struct pirrt_ctx {
     bool broken = false;
     unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
     double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
+    int bfs_async = 0;                                       // PIRRT_BFS=async: barrier-free work-queue Evaluate (experimental)
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
 };
 
@@ -172,8 +174,17 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
         if (c->stamp_cap > old_cap)   // fresh slots must read as "never visited"
             CU(cudaMemsetAsync(c->stamp + n, 0, (size_t)(c->stamp_cap - n) * sizeof(unsigned), s));
     }
-    if ((rc = grow(c->Bq[c->Bsel], c->Bq_cap[c->Bsel], cap + 1, 1 + c->Bcount, s))) return rc;
-    if ((rc = grow(c->Bq[1 - c->Bsel], c->Bq_cap[1 - c->Bsel], cap + 1, 1, s))) return rc;
+    for (int k = 0; k < 2; ++k) {
+        // list buffers: slots beyond the live entries are -1 (work-queue invariant)
+        const int64_t keep = (k == c->Bsel) ? 1 + c->Bcount : 1;
+        const int64_t old_cap = c->Bq_cap[k];
+        if ((rc = grow(c->Bq[k], c->Bq_cap[k], cap + 2, keep, s))) return rc;
+        if (c->Bq_cap[k] != old_cap) {
+            CU(cudaMemsetAsync(c->Bq[k] + keep, 0xFF, (size_t)(c->Bq_cap[k] - keep) * sizeof(int), s));
+            if (old_cap == 0) CU(cudaMemsetAsync(c->Bq[k], 0, sizeof(int), s));   // slot 0 = root
+        }
+    }
+    if ((rc = grow(c->qdepth, c->qdepth_cap, cap + 2, 0, s))) return rc;
     if ((rc = grow(c->path, c->path_cap, cap + 2, 0, s))) return rc;
     c->vcap = cap;
     return 0;
@@ -184,7 +195,7 @@ void free_all(pirrt_ctx* c) {
                     c->sboff, c->sbidx, c->sbcost, c->soboff, c->sobidx,
                     c->doff[0], c->doff[1], c->didx[0], c->didx[1], c->dcost[0], c->dcost[1],
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
-                    c->stamp, c->Bq[0], c->Bq[1], c->path, c->cnt, c->scan_tmp, c->ctl,
+                    c->stamp, c->Bq[0], c->Bq[1], c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -291,6 +302,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_WATCHDOG_MS"))
         c->watchdog_ns = (unsigned long long)std::strtoull(w, nullptr, 10) * 1000000ull;
     if (const char* w = std::getenv("PIRRT_COMPACT_MIN")) c->compact_min = std::atof(w);
+    if (const char* w = std::getenv("PIRRT_BFS")) c->bfs_async = std::strcmp(w, "async") == 0;
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -340,8 +352,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         cudaMemsetAsync(c->doff[0], 0, 3 * sizeof(long long), s) != cudaSuccess ||
         cudaMemsetAsync(c->oboff, 0, 3 * sizeof(long long), s) != cudaSuccess ||
         cudaMemsetAsync(c->odoff[0], 0, 3 * sizeof(long long), s) != cudaSuccess ||
-        cudaMemsetAsync(c->Bq[0], 0, sizeof(int), s) != cudaSuccess ||   // Bq[k][0] = root = 0
-        cudaMemsetAsync(c->Bq[1], 0, sizeof(int), s) != cudaSuccess ||
+
         cudaMemsetAsync(c->ctl, 0, sizeof(DevCtl), s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "create: init copies"));
@@ -460,6 +471,9 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     a.eps = c->cfg.epsilon;
     a.prune_off = (c->cfg.flags & PIRRT_F_PRUNE_OFF) ? 1 : 0;
     a.watchdog_ns = c->watchdog_ns;
+    a.bfs_async = c->bfs_async;
+    a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
+    a.qdepth = c->qdepth;
     CU(cudaEventRecord(c->ev0, s));
     const long long l0 = g_kernel_launches;
     cudaError_t e = launch_exploit(a, c->grid_blocks, s);
@@ -607,7 +621,10 @@ int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, con
     } else {
         CU(cudaMemsetAsync(c->b, 0, (size_t)n, s));
     }
-    // the B list is the device-side representation of b
+    // the B list is the device-side representation of b;
+    // both list buffers restart from the all -1 state
+    for (int k = 0; k < 2; ++k)
+        CU(cudaMemsetAsync(c->Bq[k] + 1, 0xFF, (size_t)(c->Bq_cap[k] - 1) * sizeof(int), s));
     int* cnt_dev = c->path + (c->path_cap - 1);
     const long long l1 = g_kernel_launches;
     CU(launch_rebuild_blist(c->b, n, c->Bq[c->Bsel], cnt_dev, c->cnt, c->scan_tmp, s));

@@ -32,6 +32,8 @@ struct IterCtl {
     int g_changed;                // some g bit changed in Evaluate
     int both;                     // |old B  n  new B|
     int lpush[3];                 // expanded vertices per BFS level (rotating slots)
+    int qpushed;                  // async BFS: items pushed after the root
+    int qdone;                    // async BFS: items processed (flushed lazily)
     int lvis[3];                  // "some child visited" per BFS level (rotating slots)
 };
 
@@ -77,6 +79,7 @@ struct ExploitArgs {
     double* pc;
     unsigned char* b;
     unsigned* stamp;              // 2e: visited in Evaluate e; 2e+1: expanded in e
+    int* qdepth;                  // async BFS: depth of the vertex in queue slot i
     // B lists (entry 0 = root, B = [1, 1 + count)); Bq[Bsel] is current
     int* Bq0;
     int* Bq1;
@@ -89,6 +92,8 @@ struct ExploitArgs {
     double eps;
     int prune_off;
     unsigned long long watchdog_ns;   // abort the loop after this long (diagnostic guard)
+    int bfs_async;                    // 1: barrier-free work-queue Evaluate, 0: level-synchronous
+    int debug;                        // PIRRT_DEBUG: device diagnostics
 };
 
 // kernels launched by this host thread (diagnostics; abi.cu attributes the
