@@ -29,7 +29,7 @@ gen/libgen.so: gen/rrg.cpp
 
 $(LIBPIRRT): $(CU_SRCS) $(CU_HDRS)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(CU_SRCS) -lcuda 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(CU_SRCS) -ldl 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; exit 1)
 	@grep -E "registers|spill" $(PKG)/lib/ptxas.log | sed 's/^/  /' | head -40
 
 clean:

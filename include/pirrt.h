@@ -56,6 +56,7 @@ enum {
     /* config flags */
     PIRRT_F_PRUNE_OFF = 1u,        /* I = V \ {root}, thr = +inf: classical PI (test/cold mode) */
     PIRRT_F_VALIDATE = 2u,         /* extra checks: g_new consistency                           */
+    PIRRT_F_SHARDED = 16u,         /* use the sharded (NCCL) exploit loop even with nranks == 1 */
     /* append flags */
     PIRRT_F_EDGES_UNDIRECTED = 4u, /* each (src,dst,cost) is stored in both directions         */
     PIRRT_F_DEVICE_PTRS = 8u       /* input arrays are device pointers (e.g. torch CUDA tensors)*/
@@ -72,9 +73,10 @@ typedef struct {
     int32_t device;           /* CUDA device ordinal                                        */
     void* stream;             /* cudaStream_t to run on (e.g. a torch stream); NULL: own one */
     int32_t grid_blocks;      /* persistent-kernel grid; 0 = auto (SMs x occupancy)          */
-    int32_t nranks;           /* multi-GPU SPMD: ranks (1 = single GPU)                      */
+    int32_t nranks;           /* multi-GPU SPMD: ranks (1 = single GPU), one process per GPU */
     int32_t rank;             /* this process's rank                                        */
-    const void* nccl_unique_id; /* ncclUniqueId (128 B) shared by all ranks when nranks > 1  */
+    const void* nccl_unique_id; /* ncclUniqueId (128 B, pirrt_nccl_unique_id on one rank,
+                                   broadcast by the caller) when nranks > 1; NULL otherwise  */
 } pirrt_config;
 
 typedef struct {
@@ -163,6 +165,15 @@ int pirrt_set_policy(pirrt_ctx* ctx, const pirrt_vid* parent, const double* g,
 
 int64_t pirrt_num_vertices(const pirrt_ctx* ctx);
 int64_t pirrt_num_edges(const pirrt_ctx* ctx);   /* directed edges stored */
+/* Multi-GPU mode.  With nranks > 1 every rank makes
+ * the same call sequence with the same arguments (SPMD); the graph and the
+ * policy are replicated, Improve is split by vertex (v mod nranks == rank),
+ * its records are all-gathered with NCCL once per PI iteration, and every
+ * rank runs the identical Evaluate, so results are bit-identical to one GPU.
+ * Stats: relaxations / improve_set count this rank's share.
+ * pirrt_nccl_unique_id writes the 128-byte ncclUniqueId (call on one rank). */
+int pirrt_nccl_unique_id(void* out, int64_t cap);
+
 /* Number of CUDA kernels this context has launched so far (diagnostics). */
 int64_t pirrt_kernel_launches(const pirrt_ctx* ctx);
 const char* pirrt_last_error(void);              /* thread-local; valid until the next call */

@@ -4,6 +4,8 @@
 // host synchronisation at the end (for n_new_promising and the validation
 // verdict).  No CPU fallback exists: every result is computed on the device.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstddef>
@@ -66,6 +68,47 @@ std::string err_bits(int e) {
     if (e & kErrRoot) m += " root must have parent -1 and g 0;";
     return m;
 }
+
+// NCCL is loaded lazily (dlopen), only when a context is sharded: a
+// single-GPU user needs no NCCL.  If torch already loaded libnccl.so.2 the
+// same library is reused.
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi* nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+            api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+            api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+            api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+            if (api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy &&
+                api.errorString)
+                api.h = h;
+        }
+    }
+    return api.h ? &api : nullptr;
+}
+
+#define NC(call)                                                                   \
+    do {                                                                           \
+        ncclResult_t r_ = (call);                                                  \
+        if (r_ != ncclSuccess)                                                     \
+            return fail(PIRRT_E_NCCL, std::string(#call) + ": " + nccl_api()->errorString(r_)); \
+    } while (0)
 
 }  // namespace
 
@@ -131,6 +174,15 @@ struct pirrt_ctx {
     unsigned char* s_b = nullptr; int64_t s_b_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool broken = false;
+    // sharded mode (nranks > 1, or PIRRT_F_SHARDED): vertex-cyclic Improve,
+    // all-gather of the Improve records, replicated Evaluate
+    bool sharded = false;
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+    ShardRec* rec_local = nullptr; int64_t rec_local_cap = 0;
+    ShardRec* rec_all = nullptr; int64_t rec_all_cap = 0;
+    int* rec_counts = nullptr; int64_t rec_counts_cap = 0;   // [0] local count, [1..nranks] gathered
+    int shard_blocks = 0;
     unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
     double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
     int bfs_async = 0;                                       // PIRRT_BFS=async: barrier-free work-queue Evaluate (experimental)
@@ -196,13 +248,15 @@ void free_all(pirrt_ctx* c) {
                     c->doff[0], c->doff[1], c->didx[0], c->didx[1], c->dcost[0], c->dcost[1],
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
                     c->stamp, c->Bq[0], c->Bq[1], c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
-                    c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b};
+                    c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
+                    c->rec_local, c->rec_all, c->rec_counts};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->comm && nccl_api()) nccl_api()->commDestroy(c->comm);
 }
 
 template <class T>
@@ -291,8 +345,10 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (!(cfg.h_root >= 0.0) || !(cfg.h_goal >= 0.0) || std::isinf(cfg.h_root) ||
         std::isinf(cfg.h_goal) || !(cfg.epsilon >= 0.0) || cfg.max_iterations < 0)
         return fail(PIRRT_E_INVAL, "create: invalid h_root/h_goal/epsilon/max_iterations");
-    if (cfg.nranks > 1)
-        return fail(PIRRT_E_STATE, "create: multi-GPU mode (nranks > 1) is not built in this version");
+    if (cfg.nranks < 1 || cfg.rank < 0 || cfg.rank >= cfg.nranks)
+        return fail(PIRRT_E_INVAL, "create: bad nranks/rank");
+    if (cfg.nranks > 1 && !cfg.nccl_unique_id)
+        return fail(PIRRT_E_INVAL, "create: nranks > 1 needs nccl_unique_id");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (cfg.device < 0 || cfg.device >= ndev) return fail(PIRRT_E_INVAL, "create: bad device");
@@ -338,6 +394,23 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         return bail(fail(PIRRT_E_NOMEM, "ctl host"));
     if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "events"));
+    if (cfg.nranks > 1 || (cfg.flags & PIRRT_F_SHARDED)) {
+        NcclApi* api = nccl_api();
+        if (!api) return bail(fail(PIRRT_E_NCCL, "create: libnccl.so.2 not loadable"));
+        ncclUniqueId id;
+        if (cfg.nccl_unique_id) std::memcpy(&id, cfg.nccl_unique_id, sizeof(id));
+        else if (api->getUniqueId(&id) != ncclSuccess) return bail(fail(PIRRT_E_NCCL, "create: ncclGetUniqueId"));
+        if (api->commInitRank(&c->comm, cfg.nranks, id, cfg.rank) != ncclSuccess)
+            return bail(fail(PIRRT_E_NCCL, "create: ncclCommInitRank"));
+        c->sharded = true;
+        c->rank = cfg.rank;
+        c->nranks = cfg.nranks;
+        int per_sm = shard_evaluate_blocks_per_sm();
+        if (per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: shard kernel does not fit an SM"));
+        c->shard_blocks = cfg.grid_blocks > 0 ? std::min(cfg.grid_blocks, per_sm * c->num_sms)
+                                              : per_sm * c->num_sms;
+        if ((rc = grow(c->rec_counts, c->rec_counts_cap, cfg.nranks + 1, 0, c->stream))) return bail(rc);
+    }
     // V = {x_init, x_goal}, E = {}, B = {}
     const double g0[2] = {0.0, INFINITY};
     const double h0[2] = {cfg.h_root + 0.0, cfg.h_goal + 0.0};
@@ -450,13 +523,8 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     return PIRRT_OK;
 }
 
-int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
-    if (!c) return fail(PIRRT_E_INVAL, "exploit: NULL context");
-    int rc;
-    if ((rc = set_device(c))) return rc;
-    cudaStream_t s = c->stream;
-    CU(cudaMemsetAsync(c->ctl, 0, offsetof(DevCtl, err), s));
-    ExploitArgs a;
+static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
+    std::memset(&a, 0, sizeof(a));
     a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
     a.doff = c->doff[c->cur]; a.didx = c->didx[c->cur]; a.dcost = c->dcost[c->cur];
     a.oboff = c->oboff; a.obidx = c->obidx;
@@ -464,6 +532,7 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
     a.stamp = c->stamp;
     a.Bq0 = c->Bq[0]; a.Bq1 = c->Bq[1]; a.Bsel = c->Bsel; a.Bcount = c->Bcount;
+    a.old_Bcount = 0; a.pending = 0;
     a.ev_base = c->ev_next;
     a.ctl = c->ctl;
     a.n = c->n;
@@ -474,17 +543,98 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     a.bfs_async = c->bfs_async;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
     a.qdepth = c->qdepth;
+}
+
+// Sharded exploit: per PI iteration
+//   1. Improve over the owned part of I (v mod P == rank) -> records,
+//   2. ncclAllGather of the record counts, then of the records (padded),
+//   3. every rank applies all records and runs the identical Evaluate.
+// The global Delta g is the max over the gathered records: no all-reduce.
+static int exploit_sharded(pirrt_ctx* c) {
+    cudaStream_t s = c->stream;
+    NcclApi* api = nccl_api();
+    int rc;
+    ExploitArgs a;
+    fill_exploit_args(c, a);
+    a.shard_rank = c->rank;
+    a.shard_n = c->nranks;
+    const long long cap = c->cfg.max_iterations > 0 ? c->cfg.max_iterations : 10LL * c->n;
+    // records: at most one per owned vertex of I
+    if ((rc = grow(c->rec_local, c->rec_local_cap, c->n / c->nranks + 2, 0, s))) return rc;
+    a.rec_out = c->rec_local;
+    a.rec_count = c->rec_counts;
+    int Bsel = c->Bsel, Bc = c->Bcount, old_Bc = 0, pending = 0;
+    unsigned ev = c->ev_next;
+    std::vector<int> counts(c->nranks + 1);
+    for (int it = 1;; ++it) {
+        if ((long long)it > cap) {
+            if (pending) {   // finish the last Evaluate's bookkeeping, then report
+                a.Bsel = Bsel; a.Bcount = 0; a.old_Bcount = old_Bc; a.pending = 1; a.ev_base = ev;
+                a.shard_n = c->nranks;
+                CU(launch_shard_improve(a, it, c->shard_blocks, s));
+            }
+            c->Bsel = Bsel; c->Bcount = Bc;
+            c->ev_next = ev;
+            return fail(PIRRT_E_NOCONV, "exploit: iteration cap exceeded");
+        }
+        CU(cudaMemsetAsync(&c->ctl->it[it & 1], 0, sizeof(IterCtl), s));
+        CU(cudaMemsetAsync(c->rec_counts, 0, sizeof(int), s));
+        a.Bsel = Bsel; a.Bcount = Bc; a.old_Bcount = old_Bc; a.pending = pending; a.ev_base = ev;
+        CU(launch_shard_improve(a, it, c->shard_blocks, s));
+        c->launches += 1;
+        NC(api->allGather(c->rec_counts, c->rec_counts + 1, 1, ncclInt32, c->comm, s));
+        CU(cudaMemcpyAsync(counts.data(), c->rec_counts, sizeof(int) * (c->nranks + 1),
+                           cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        int stride = 1;
+        for (int r = 0; r < c->nranks; ++r) stride = std::max(stride, counts[1 + r]);
+        if ((rc = grow(c->rec_all, c->rec_all_cap, (int64_t)stride * c->nranks, 0, s))) return rc;
+        NC(api->allGather(c->rec_local, c->rec_all, (size_t)stride * sizeof(ShardRec), ncclChar,
+                          c->comm, s));
+        a.pending = 0;   // leave_B was done by the Improve kernel
+        CU(launch_shard_evaluate(a, it, c->rec_all, c->rec_counts + 1, stride, c->nranks,
+                                 c->shard_blocks, s));
+        c->launches += 1;
+        if ((rc = read_ctl(c))) return rc;
+        const DevCtl& h = *c->ctl_host;
+        Bsel = h.Bsel_out; Bc = h.Bcount_out; old_Bc = h.old_Bcount_out; pending = h.pending_out;
+        ev = c->ev_next + (unsigned)h.evaluations;
+        if (h.abort_at) break;
+        if (h.shard_stop) break;
+    }
+    c->Bsel = Bsel;
+    c->Bcount = Bc;
+    c->ev_next = ev;
+    return 0;
+}
+
+int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
+    if (!c) return fail(PIRRT_E_INVAL, "exploit: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    cudaStream_t s = c->stream;
+    CU(cudaMemsetAsync(c->ctl, 0, offsetof(DevCtl, err), s));
     CU(cudaEventRecord(c->ev0, s));
-    const long long l0 = g_kernel_launches;
-    cudaError_t e = launch_exploit(a, c->grid_blocks, s);
-    c->launches += g_kernel_launches - l0;
-    if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
-    CU(cudaEventRecord(c->ev1, s));
-    if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+    int xrc = 0;
+    if (c->sharded) {
+        xrc = exploit_sharded(c);
+        if (xrc != 0 && xrc != PIRRT_E_NOCONV) { c->broken = true; return xrc; }
+        CU(cudaEventRecord(c->ev1, s));
+        if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+    } else {
+        ExploitArgs a;
+        fill_exploit_args(c, a);
+        const long long l0 = g_kernel_launches;
+        cudaError_t e = launch_exploit(a, c->grid_blocks, s);
+        c->launches += g_kernel_launches - l0;
+        if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
+        CU(cudaEventRecord(c->ev1, s));
+        if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+        c->Bsel = c->ctl_host->Bsel_out;
+        c->Bcount = c->ctl_host->Bcount_out;
+        c->ev_next += (unsigned)c->ctl_host->evaluations;
+    }
     const DevCtl& h = *c->ctl_host;
-    c->Bsel = h.Bsel_out;
-    c->Bcount = h.Bcount_out;
-    c->ev_next += (unsigned)h.evaluations;
     if (st) {
         std::memset(st, 0, sizeof(*st));
         st->iterations = h.iterations;
@@ -495,13 +645,12 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
         st->max_level = h.max_level;
         st->promising = h.promising;
         st->stalled = h.stalled;
-        st->grid_blocks = c->grid_blocks;
+        st->grid_blocks = c->sharded ? c->shard_blocks : c->grid_blocks;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
         st->device_ms = ms;
         st->improve_ms = (float)(h.t_improve * 1e-6);
         st->evaluate_ms = (float)(h.t_evaluate * 1e-6);
-
         st->improve_set = h.improve_set;
         st->eval_scanned = h.eval_scanned;
         st->barriers = h.barriers;
@@ -510,7 +659,18 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
         c->broken = true;
         return fail(PIRRT_E_STATE, "exploit: watchdog fired (PIRRT_WATCHDOG_MS); context unusable");
     }
-    if (h.status == PIRRT_E_NOCONV) return fail(PIRRT_E_NOCONV, "exploit: iteration cap exceeded");
+    if (xrc == PIRRT_E_NOCONV || h.status == PIRRT_E_NOCONV)
+        return fail(PIRRT_E_NOCONV, "exploit: iteration cap exceeded");
+    return PIRRT_OK;
+}
+
+int pirrt_nccl_unique_id(void* out, int64_t cap) {
+    if (!out || cap < (int64_t)sizeof(ncclUniqueId)) return fail(PIRRT_E_RANGE, "nccl_unique_id: need 128 bytes");
+    NcclApi* api = nccl_api();
+    if (!api) return fail(PIRRT_E_NCCL, "nccl_unique_id: libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    NC(api->getUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
     return PIRRT_OK;
 }
 

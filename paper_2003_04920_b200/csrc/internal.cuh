@@ -37,6 +37,12 @@ struct IterCtl {
     int lvis[3];                  // "some child visited" per BFS level (rotating slots)
 };
 
+// One Improve result in sharded mode (all-gathered between ranks).
+struct ShardRec {
+    int v, parent, changed, pad;
+    double pc, delta;
+};
+
 // Device control block (one per context, cudaMalloc'ed, 8-byte aligned).
 // Everything up to `err` is zeroed before each exploit.
 struct DevCtl {
@@ -45,6 +51,8 @@ struct DevCtl {
     int status;                   // 0 ok, PIRRT_E_NOCONV
     int iterations, evaluations, max_level, promising, stalled;
     int Bsel_out, Bcount_out;     // B list after the exploit
+    int old_Bcount_out, pending_out;  // pending leave_B (sharded host loop)
+    int shard_stop;               // sharded: 0 continue, 1 converged, 2 stalled/aborted
     int barriers;
     int abort_at;                 // watchdog: barrier index at which all threads stop
     double last_dg;
@@ -85,7 +93,12 @@ struct ExploitArgs {
     int* Bq1;
     int Bsel;
     int Bcount;
+    int old_Bcount;               // previous list still awaiting leave_B (sharded loop)
+    int pending;
     unsigned ev_base;             // id of this exploit's first Evaluate
+    int shard_rank, shard_n;      // sharded Improve: owned vertices v % shard_n == shard_rank
+    ShardRec* rec_out;            // sharded Improve records
+    int* rec_count;
     DevCtl* ctl;
     int n;
     int max_it;
@@ -102,7 +115,12 @@ extern thread_local long long g_kernel_launches;
 
 // ---- launchers (store.cu / exploit.cu) ----
 cudaError_t launch_exploit(const ExploitArgs& a, int blocks, cudaStream_t s);
+cudaError_t launch_shard_improve(const ExploitArgs& a, int it, int blocks, cudaStream_t s);
+cudaError_t launch_shard_evaluate(const ExploitArgs& a, int it, const ShardRec* recs,
+                                  const int* counts, int stride, int nranks, int blocks,
+                                  cudaStream_t s);
 int exploit_blocks_per_sm();
+int shard_evaluate_blocks_per_sm();
 
 struct AppendArgs {
     // committed store (read)

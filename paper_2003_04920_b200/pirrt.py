@@ -35,13 +35,15 @@ PIRRT_F_PRUNE_OFF = 1
 PIRRT_F_VALIDATE = 2
 PIRRT_F_EDGES_UNDIRECTED = 4
 PIRRT_F_DEVICE_PTRS = 8
+PIRRT_F_SHARDED = 16
+NCCL_UNIQUE_ID_BYTES = 128
 
 # every symbol include/pirrt.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "pirrt_config_init", "pirrt_create", "pirrt_destroy", "pirrt_graph_append_batch",
     "pirrt_exploit", "pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
     "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
-    "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error",
+    "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id",
 )
 
 
@@ -108,6 +110,7 @@ def _load():
     lib.pirrt_kernel_launches.argtypes = [P]
     lib.pirrt_kernel_launches.restype = C.c_int64
     lib.pirrt_last_error.restype = C.c_char_p
+    lib.pirrt_nccl_unique_id.argtypes = [P, C.c_int64]
     return lib
 
 
@@ -129,6 +132,14 @@ pirrt_num_vertices = _lib.pirrt_num_vertices
 pirrt_num_edges = _lib.pirrt_num_edges
 pirrt_kernel_launches = _lib.pirrt_kernel_launches
 pirrt_last_error = _lib.pirrt_last_error
+pirrt_nccl_unique_id = _lib.pirrt_nccl_unique_id
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for a sharded context group."""
+    buf = C.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    _check(pirrt_nccl_unique_id(buf, NCCL_UNIQUE_ID_BYTES))
+    return buf.raw
 
 
 class PirrtError(RuntimeError):
@@ -169,13 +180,19 @@ class Context:
     """One exploitation context (vertices 0 = x_init and 1 = x_goal exist)."""
 
     def __init__(self, h_root=0.0, h_goal=0.0, epsilon=0.0, max_iterations=0, flags=0, device=0,
-                 stream=None, vertex_capacity=0, edge_capacity=0, grid_blocks=0):
+                 stream=None, vertex_capacity=0, edge_capacity=0, grid_blocks=0, nranks=1,
+                 rank=0, nccl_id: bytes | None = None):
         cfg = pirrt_config()
         pirrt_config_init(C.byref(cfg))
         cfg.h_root, cfg.h_goal, cfg.epsilon = float(h_root), float(h_goal), float(epsilon)
         cfg.max_iterations, cfg.flags, cfg.device = int(max_iterations), int(flags), int(device)
         cfg.vertex_capacity, cfg.edge_capacity = int(vertex_capacity), int(edge_capacity)
         cfg.grid_blocks = int(grid_blocks)
+        cfg.nranks, cfg.rank = int(nranks), int(rank)
+        self._nccl_id = None
+        if nccl_id is not None:
+            self._nccl_id = C.create_string_buffer(bytes(nccl_id), NCCL_UNIQUE_ID_BYTES)
+            cfg.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p)
         if stream is not None:
             cfg.stream = int(getattr(stream, "cuda_stream", stream))
         h = C.c_void_p()

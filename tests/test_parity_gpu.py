@@ -255,3 +255,31 @@ def test_noconv_cap(P):
     with pytest.raises(P.PirrtError) as ei:
         gpu.exploit()
     assert ei.value.code == P.PIRRT_E_NOCONV
+
+
+# ------------------------------------------------------------------ sharded / async paths
+
+@pytest.mark.parametrize("flags", [0, PRUNE_OFF])
+def test_sharded_loop_single_rank_parity(P, flags):
+    # the multi-GPU code path (vertex-split Improve -> ncclAllGather of the
+    # records -> replicated Evaluate) with one rank: bit-identical to the oracle
+    r = gen.rrg(2, 3000, gen.gamma_star(2), n_boxes=20, seed=gen.seed_of("shard", flags))
+    gpu = P.Context(h_root=r.h_root(), flags=flags | P.PIRRT_F_SHARDED)
+    orc = Oracle(h_root=r.h_root(), flags=flags)
+    dual_replay(gpu, orc, r, 97)
+
+
+def test_sharded_loop_6d(P):
+    r = gen.rrg(6, 15000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("shard6"))
+    gpu = P.Context(h_root=r.h_root(), flags=P.PIRRT_F_SHARDED)
+    orc = Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, 1000)
+
+
+def test_async_evaluate_parity(P, monkeypatch):
+    # the barrier-free work-queue Evaluate (PIRRT_BFS=async) must agree too
+    monkeypatch.setenv("PIRRT_BFS", "async")
+    r = gen.rrg(2, 4000, gen.gamma_star(2), n_boxes=25, seed=gen.seed_of("async"))
+    gpu = P.Context(h_root=r.h_root())
+    orc = Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, 50)
