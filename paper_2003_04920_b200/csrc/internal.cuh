@@ -58,6 +58,7 @@ struct DevCtl {
     double last_dg;
     long long relaxations, eval_visits, improve_set, eval_scanned;
     unsigned long long t_improve, t_evaluate;
+    unsigned long long dbg_work_ns;   // PIRRT_DEBUG level trace
     // append / set_policy
     int err;                      // bitmask of kErr*
     int nprom;                    // new promising vertices
