@@ -185,7 +185,9 @@ struct pirrt_ctx {
     int shard_blocks = 0;
     unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
     double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
-    int bfs_async = 0;                                       // PIRRT_BFS=async: barrier-free work-queue Evaluate (experimental)
+    int bfs_async = 0;
+    int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
+    long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;                                       // PIRRT_BFS=async: barrier-free work-queue Evaluate (experimental)
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
 };
 
@@ -249,7 +251,7 @@ void free_all(pirrt_ctx* c) {
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
                     c->stamp, c->Bq[0], c->Bq[1], c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
-                    c->rec_local, c->rec_all, c->rec_counts};
+                    c->rec_local, c->rec_all, c->rec_counts, c->app_bsum};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
@@ -303,10 +305,10 @@ int fold(pirrt_ctx* c, long long*& boff, int64_t& boff_cap, int*& bidx, int64_t&
 }
 
 int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
-    // fold the deltas into the bases when they outgrow sqrt(8 m |base|) (and
-    // 32k edges): the per-append merge cost O(delta) balances the amortised
-    // O(|E|) fold
-    double thr = std::sqrt(8.0 * (double)std::max<int64_t>(m_dir, 1) * (double)c->base_edges);
+    // fold the deltas into the bases when they outgrow sqrt(2 m |base|) (and
+    // 32k edges): minimises (mean delta copied per append) + (|E| fold cost
+    // amortised over the appends between folds)
+    double thr = std::sqrt(2.0 * (double)std::max<int64_t>(m_dir, 1) * (double)c->base_edges);
     thr = std::max(thr, c->compact_min);
     if ((double)c->delta_edges <= thr) return 0;
     const int64_t E = c->base_edges + c->delta_edges;
@@ -359,6 +361,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         c->watchdog_ns = (unsigned long long)std::strtoull(w, nullptr, 10) * 1000000ull;
     if (const char* w = std::getenv("PIRRT_COMPACT_MIN")) c->compact_min = std::atof(w);
     if (const char* w = std::getenv("PIRRT_BFS")) c->bfs_async = std::strcmp(w, "async") == 0;
+    if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -387,6 +390,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if ((rc = grow(c->bidx, c->bidx_cap, 64, 0, c->stream))) return bail(rc);
     if ((rc = grow(c->bcost, c->bcost_cap, 64, 0, c->stream))) return bail(rc);
     if ((rc = grow(c->obidx, c->obidx_cap, 64, 0, c->stream))) return bail(rc);
+    if ((rc = grow(c->app_bsum, c->app_bsum_cap, 2 * kAppendMaxBlocks + 2, 0, c->stream))) return bail(rc);
     for (int k = 0; k < 2; ++k)
         if ((rc = grow(c->odidx[k], c->odidx_cap[k], ecap0, 0, c->stream))) return bail(rc);
     if (cudaMalloc(&c->ctl, sizeof(DevCtl)) != cudaSuccess) return bail(fail(PIRRT_E_NOMEM, "ctl"));
@@ -504,7 +508,9 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     a.ctl = c->ctl;
     a.grid_blocks = c->num_sms;
     const long long l0 = g_kernel_launches;
-    cudaError_t e = launch_append(a, s);
+    cudaError_t e = c->fused_append
+        ? launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks, s)
+        : launch_append(a, s);
     c->launches += g_kernel_launches - l0;
     if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("append: ") + cudaGetErrorString(e)); }
     if ((rc = read_ctl(c))) { c->broken = true; return rc; }

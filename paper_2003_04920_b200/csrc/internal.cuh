@@ -154,6 +154,10 @@ struct AppendArgs {
     int grid_blocks;
 };
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t s);
+// one cooperative kernel for the whole append; bsum needs 2 * max_blocks entries
+cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
+                                int max_blocks, cudaStream_t s);
+constexpr int kAppendMaxBlocks = 2048;
 
 // fold a delta CSR into its base CSR (cost arrays may be NULL: out-index)
 struct CompactArgs {

@@ -172,28 +172,25 @@ __global__ void k_edge_hist(const int* src, const int* dst, long long m, int und
     }
 }
 
-// warp per row: copy the old delta row to its new position; leave the row's
-// write cursor in cnt[v]
+// thread per row (delta rows are short): copy the old delta row to its new
+// position and leave the row's write cursor in cursor[v]
 __global__ void k_delta_copy_old(const long long* doff_old, const int* didx_old,
                                  const double* dcost_old, const long long* doff_new, int* didx_new,
                                  double* dcost_new, int n_old, int n_all, long long* cursor,
                                  const DevCtl* ctl) {
     if (failed(ctl)) return;
-    const int lane = threadIdx.x & 31;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int v = w; v < n_all; v += nw) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n_all; v += gridDim.x * blockDim.x) {
         const long long dst0 = doff_new[v];
         long long len = 0;
         if (v < n_old) {
-            const long long s0 = doff_old[v], s1 = doff_old[v + 1];
-            len = s1 - s0;
-            for (long long k = lane; k < len; k += 32) {
+            const long long s0 = doff_old[v];
+            len = doff_old[v + 1] - s0;
+            for (long long k = 0; k < len; ++k) {
                 didx_new[dst0 + k] = didx_old[s0 + k];
                 if (dcost_new) dcost_new[dst0 + k] = dcost_old[s0 + k];
             }
         }
-        if (lane == 0) cursor[v] = dst0 + len;
+        cursor[v] = dst0 + len;
     }
 }
 
@@ -442,6 +439,287 @@ __global__ void k_best_path(const int* parent, int n, int* path_rev, int* len_ou
     *len_out = (v == -1) ? len : -1;   // -1: cycle
 }
 
+
+// ------------------------------------------------------------------ fused append
+// One cooperative launch for the whole append (row a1): validation, the
+// counting-sort merge of the batch into both delta stores (in-edge rows with
+// costs, out-edge ids), base-row extension, new-vertex init, Extend's local
+// relaxation (R14) or the given policy's edge costs, and the promising test.
+// Grid barriers replace ~20 dependent kernel launches.
+
+__device__ __forceinline__ long long blk_sum_ll(long long x, long long* sm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    __syncthreads();
+    if (lane == 0) sm[w] = x;
+    __syncthreads();
+    long long t = 0;
+    for (int i = 0; i < kBT / 32; ++i) t += sm[i];
+    return t;                                            // every thread
+}
+
+// exclusive block scan of one long long per thread; *total = block sum
+__device__ __forceinline__ long long blk_excl_scan_ll(long long x, long long* sm, long long* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long inc = x;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += y;
+    }
+    __syncthreads();
+    if (lane == 31) sm[w] = inc;
+    __syncthreads();
+    long long before = 0, all = 0;
+    for (int i = 0; i < kBT / 32; ++i) {
+        if (i < w) before += sm[i];
+        all += sm[i];
+    }
+    *total = all;
+    return before + inc - x;
+}
+
+__global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* cnt1,
+                                                      long long* bsum) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ long long sm[kBT / 32];
+    DevCtl* ctl = a.ctl;
+    const int n_old = a.n_old, n_new = a.n_new, n_all = n_old + n_new;
+    const long long m = a.m;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nthreads = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int gw = tid >> 5, nw = nthreads >> 5;
+    long long* cnt0 = a.cnt;
+    // ---- P0 validation (R12)
+    {
+        int err = 0;
+        for (long long e = tid; e < m; e += nthreads) {
+            const int sv = a.src[e], dv = a.dst[e];
+            const double c = a.cost[e];
+            if (sv < 0 || sv >= n_all || dv < 0 || dv >= n_all) err |= kErrRange;
+            else if (sv == dv) err |= kErrSelfLoop;
+            if (!(c >= 0.0) || isinf(c)) err |= kErrCost;
+        }
+        for (int i = tid; i < n_new; i += nthreads) {
+            const double hv = a.h_in[i];
+            if (!(hv >= 0.0) || isinf(hv)) err |= kErrH;
+            if (a.parent_in) {
+                const int pp = a.parent_in[i];
+                const double gv = a.g_in[i];
+                if (pp < -1 || pp >= n_all || pp == n_old + i) err |= kErrRange;
+                else if (pp < 0 && !isinf(gv)) err |= kErrGNew;
+                else if (pp >= 0 && (!(gv >= 0.0) || isinf(gv))) err |= kErrGNew;
+            }
+        }
+        if (err) atomicOr(&ctl->err, err);
+    }
+    grid.sync();
+    if (failed(ctl)) return;                              // uniform: err is final
+    // ---- P1 old delta row lengths (both stores)
+    for (int v = tid; v <= n_all; v += nthreads) {
+        cnt0[v] = v < n_old ? a.doff_old[v + 1] - a.doff_old[v] : 0;
+        cnt1[v] = v < n_old ? a.odoff_old[v + 1] - a.odoff_old[v] : 0;
+    }
+    grid.sync();
+    // ---- P2 histogram of the new edges by row
+    for (long long e = tid; e < m; e += nthreads) {
+        const int sv = a.src[e], dv = a.dst[e];
+        atomicAdd((unsigned long long*)&cnt0[dv], 1ull);
+        atomicAdd((unsigned long long*)&cnt1[sv], 1ull);
+        if (a.undirected) {
+            atomicAdd((unsigned long long*)&cnt0[sv], 1ull);
+            atomicAdd((unsigned long long*)&cnt1[dv], 1ull);
+        }
+    }
+    grid.sync();
+    // ---- P3 exclusive scans -> new delta row offsets (chunk per block)
+    const int G = gridDim.x;
+    const int chunk = (n_all + G - 1) / G;
+    const int c0 = min(n_all, (int)blockIdx.x * chunk), c1 = min(n_all, c0 + chunk);
+    {
+        long long s0 = 0, s1 = 0;
+        for (int v = c0 + threadIdx.x; v < c1; v += kBT) { s0 += cnt0[v]; s1 += cnt1[v]; }
+        s0 = blk_sum_ll(s0, sm);
+        s1 = blk_sum_ll(s1, sm);
+        if (threadIdx.x == 0) { bsum[blockIdx.x] = s0; bsum[G + blockIdx.x] = s1; }
+    }
+    grid.sync();
+    {
+        long long p0 = 0, p1 = 0, t0 = 0, t1 = 0;
+        for (int i = threadIdx.x; i < G; i += kBT) {
+            const long long x0 = bsum[i], x1 = bsum[G + i];
+            if (i < (int)blockIdx.x) { p0 += x0; p1 += x1; }
+            t0 += x0; t1 += x1;
+        }
+        p0 = blk_sum_ll(p0, sm); p1 = blk_sum_ll(p1, sm);
+        t0 = blk_sum_ll(t0, sm); t1 = blk_sum_ll(t1, sm);
+        for (int base = c0; base < c1; base += kBT) {
+            const int v = base + threadIdx.x;
+            const long long x0 = v < c1 ? cnt0[v] : 0, x1 = v < c1 ? cnt1[v] : 0;
+            long long tot0, tot1;
+            const long long o0 = blk_excl_scan_ll(x0, sm, &tot0);
+            const long long o1 = blk_excl_scan_ll(x1, sm, &tot1);
+            if (v < c1) { a.doff_new[v] = p0 + o0; a.odoff_new[v] = p1 + o1; }
+            p0 += tot0; p1 += tot1;
+        }
+        if (tid == 0) { a.doff_new[n_all] = t0; a.odoff_new[n_all] = t1; }
+    }
+    grid.sync();
+    // ---- P4 copy the old delta rows (thread per row), leave cursors; base
+    //      rows of the new vertices are empty
+    for (int v = tid; v < n_all; v += nthreads) {
+        const long long d0 = a.doff_new[v], e0 = a.odoff_new[v];
+        long long len0 = 0, len1 = 0;
+        if (v < n_old) {
+            const long long s0 = a.doff_old[v];
+            len0 = a.doff_old[v + 1] - s0;
+            for (long long k = 0; k < len0; ++k) {
+                a.didx_new[d0 + k] = a.didx_old[s0 + k];
+                a.dcost_new[d0 + k] = a.dcost_old[s0 + k];
+            }
+            const long long s1 = a.odoff_old[v];
+            len1 = a.odoff_old[v + 1] - s1;
+            for (long long k = 0; k < len1; ++k) a.odidx_new[e0 + k] = a.odidx_old[s1 + k];
+        }
+        cnt0[v] = d0 + len0;
+        cnt1[v] = e0 + len1;
+    }
+    for (int v = n_old + 1 + tid; v <= n_all; v += nthreads) {
+        a.boff_w[v] = a.base_edges;
+        a.oboff_w[v] = a.obase_edges;
+    }
+    grid.sync();
+    // ---- P5 scatter the new edges; init the new vertices
+    for (long long e = tid; e < m; e += nthreads) {
+        const int sv = a.src[e], dv = a.dst[e];
+        const double c = a.cost[e] + 0.0;                // -0.0 -> +0.0 (R12)
+        long long p = (long long)atomicAdd((unsigned long long*)&cnt0[dv], 1ull);
+        a.didx_new[p] = sv; a.dcost_new[p] = c;
+        p = (long long)atomicAdd((unsigned long long*)&cnt1[sv], 1ull);
+        a.odidx_new[p] = dv;
+        if (a.undirected) {
+            p = (long long)atomicAdd((unsigned long long*)&cnt0[sv], 1ull);
+            a.didx_new[p] = dv; a.dcost_new[p] = c;
+            p = (long long)atomicAdd((unsigned long long*)&cnt1[dv], 1ull);
+            a.odidx_new[p] = sv;
+        }
+    }
+    for (int i = tid; i < n_new; i += nthreads) {
+        const int v = n_old + i;
+        a.h[v] = a.h_in[i] + 0.0;
+        if (a.parent_in) { a.parent[v] = a.parent_in[i]; a.g[v] = a.g_in[i] + 0.0; }
+        else { a.parent[v] = -1; a.g[v] = INFINITY; }
+        a.pc[v] = 0.0;
+        a.b[v] = 0;
+    }
+    grid.sync();
+    // ---- P6 policy of the new vertices
+    if (a.parent_in) {
+        // given policy: pc(v) = cost of the stored edge (parent -> v)
+        for (int i = gw; i < n_new; i += nw) {
+            const int v = n_old + i;
+            const int p = a.parent[v];
+            if (p < 0) continue;
+            long long best = LLONG_MAX;
+            double c = 0.0;
+            for (long long k = a.boff[v] + lane; k < a.boff[v + 1]; k += 32)
+                if (a.bidx[k] == p && k < best) { best = k; c = a.bcost[k]; }
+            for (long long k = a.doff_new[v] + lane; k < a.doff_new[v + 1]; k += 32)
+                if (a.didx_new[k] == p && (1LL << 62) + k < best) { best = (1LL << 62) + k; c = a.dcost_new[k]; }
+            for (int o = 16; o; o >>= 1) {
+                const long long ob = __shfl_xor_sync(kFull, best, o);
+                const double oc = __shfl_xor_sync(kFull, c, o);
+                if (ob < best) { best = ob; c = oc; }
+            }
+            if (lane == 0) {
+                if (best == LLONG_MAX) atomicOr(&ctl->err, kErrPcMissing);
+                else {
+                    a.pc[v] = c;
+                    if (a.validate && a.g[v] != a.g[p] + c) atomicOr(&ctl->err, kErrGNew);
+                }
+            }
+        }
+    } else if (n_new > 0) {
+        // Extend's local relaxation (R14): chaotic in-place sweeps
+        // over the new vertices until a full sweep changes no (g, parent) pair;
+        // every dependency goes from a lower to a higher id, so the fixed point
+        // is unique and equals the sequential id-order result bit for bit.
+        const bool lead = tid == 0;
+        for (int sw = 0;; ++sw) {
+            int* chg = &ctl->sweep_changed[sw & 1];
+            if (lead) ctl->sweep_changed[(sw + 1) & 1] = 0;
+            bool my_change = false;
+            for (int i = gw; i < n_new; i += nw) {
+                const int v = n_old + i;
+                double best = INFINITY;
+                int arg = INT_MAX;
+                double argc = 0.0;
+                for (long long k = a.boff[v] + lane; k < a.boff[v + 1]; k += 32) {
+                    const int u = a.bidx[k];
+                    if (u >= v) continue;
+                    const double c = a.bcost[k];
+                    const double cand = *(volatile const double*)&a.g[u] + c;
+                    if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
+                }
+                for (long long k = a.doff_new[v] + lane; k < a.doff_new[v + 1]; k += 32) {
+                    const int u = a.didx_new[k];
+                    if (u >= v) continue;
+                    const double c = a.dcost_new[k];
+                    const double cand = *(volatile const double*)&a.g[u] + c;
+                    if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
+                }
+                double wb = best;
+                int wa = arg;
+                for (int o = 16; o; o >>= 1) {
+                    const double ob = __shfl_xor_sync(kFull, wb, o);
+                    const int oa = __shfl_xor_sync(kFull, wa, o);
+                    if (ob < wb || (ob == wb && oa < wa)) { wb = ob; wa = oa; }
+                }
+                const unsigned mm = __ballot_sync(kFull, best == wb && arg == wa);
+                const double c = __shfl_sync(kFull, argc, __ffs(mm) - 1);
+                if (lane == 0) {
+                    int np;
+                    double ng, npc;
+                    if (wb < INFINITY) { np = wa; ng = wb; npc = c; }
+                    else { np = -1; ng = INFINITY; npc = 0.0; }
+                    if (np != a.parent[v] || __double_as_longlong(ng) != __double_as_longlong(*(volatile double*)&a.g[v])) {
+                        *(volatile double*)&a.g[v] = ng;
+                        a.parent[v] = np;
+                        a.pc[v] = npc;
+                        my_change = true;
+                    }
+                }
+            }
+            if (my_change) atomicOr(chg, 1);
+            grid.sync();
+            const int any = *(volatile int*)chg;
+            if (lead) ctl->sweeps = sw + 1;
+            if (!any) break;
+            grid.sync();   // everyone has read chg before it is reset two sweeps later
+        }
+    }
+    grid.sync();
+    if (failed(ctl)) return;
+    // ---- P7 b(v) = g(v) + h(v) < g(x_goal); promising ones join the B list
+    const double thr = a.g[kGoal];
+    for (int base = blockIdx.x * blockDim.x; base < n_new; base += nthreads) {
+        const int i = base + threadIdx.x;
+        const int v = n_old + i;
+        const bool p = (i < n_new) && (a.g[v] + a.h[v] < thr);
+        if (i < n_new) a.b[v] = p ? 1 : 0;
+        const unsigned mm = __ballot_sync(kFull, p);
+        if (mm) {
+            const int leader = __ffs(mm) - 1;
+            int pos = 0;
+            if (lane == leader) pos = atomicAdd(&ctl->nprom, __popc(mm));
+            pos = __shfl_sync(kFull, pos, leader);
+            unsigned lt;
+            asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
+            if (p) a.Blist[1 + a.Bcount + pos + __popc(mm & lt)] = v;
+        }
+    }
+}
+
 }  // namespace
 
 thread_local long long g_kernel_launches = 0;
@@ -495,7 +773,7 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
         }
         if ((e = scan_exclusive(a.cnt, doff_new, n_all, a.scan_tmp, s)) != cudaSuccess) return e;
         ++g_kernel_launches;
-        k_delta_copy_old<<<grid_for((long long)n_all * 32), kBT, 0, s>>>(
+        k_delta_copy_old<<<grid_for(n_all), kBT, 0, s>>>(
             doff_old, didx_old, dcost_old, doff_new, didx_new, dcost_new, a.n_old, n_all, a.cnt,
             a.ctl);
         if (m > 0) {
@@ -548,6 +826,20 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
                                                           a.Bcount, a.ctl);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
+                                int max_blocks, cudaStream_t s) {
+    static int per_sm = -1;
+    if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_append_fused, kBT, 0);
+    int blocks = per_sm * (a.grid_blocks > 0 ? a.grid_blocks : 148);
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    AppendArgs args = a;
+    void* params[] = {&args, &cnt1, &bsum};
+    ++g_kernel_launches;
+    return cudaLaunchCooperativeKernel((const void*)k_append_fused, dim3(blocks), dim3(kBT), params,
+                                       0, s);
 }
 
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {

@@ -283,3 +283,12 @@ def test_async_evaluate_parity(P, monkeypatch):
     gpu = P.Context(h_root=r.h_root())
     orc = Oracle(h_root=r.h_root())
     dual_replay(gpu, orc, r, 50)
+
+
+def test_split_append_path_parity(P, monkeypatch):
+    # the multi-kernel append (PIRRT_APPEND=split) must agree with the fused one
+    monkeypatch.setenv("PIRRT_APPEND", "split")
+    r = gen.rrg(4, 5000, gen.gamma_k(4), n_boxes=10, seed=gen.seed_of("split"))
+    gpu = P.Context(h_root=r.h_root())
+    orc = Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, 333)
