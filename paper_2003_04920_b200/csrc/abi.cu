@@ -239,7 +239,7 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
         }
     }
     if ((rc = grow(c->qdepth, c->qdepth_cap, cap + 2, 0, s))) return rc;
-    if ((rc = grow(c->path, c->path_cap, cap + 2, 0, s))) return rc;
+    if ((rc = grow(c->path, c->path_cap, cap + 8, 0, s))) return rc;
     c->vcap = cap;
     return 0;
 }
@@ -387,9 +387,17 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         if ((rc = grow(c->didx[k], c->didx_cap[k], ecap0, 0, c->stream))) return bail(rc);
         if ((rc = grow(c->dcost[k], c->dcost_cap[k], ecap0, 0, c->stream))) return bail(rc);
     }
-    if ((rc = grow(c->bidx, c->bidx_cap, 64, 0, c->stream))) return bail(rc);
-    if ((rc = grow(c->bcost, c->bcost_cap, 64, 0, c->stream))) return bail(rc);
-    if ((rc = grow(c->obidx, c->obidx_cap, 64, 0, c->stream))) return bail(rc);
+    // base and spare base stores: reserve the caller's edge-capacity hint up
+    // front so that folds in steady state never allocate
+    const int64_t bcap0 = std::max<int64_t>(cfg.edge_capacity, 64);
+    if ((rc = grow(c->bidx, c->bidx_cap, bcap0, 0, c->stream))) return bail(rc);
+    if ((rc = grow(c->bcost, c->bcost_cap, bcap0, 0, c->stream))) return bail(rc);
+    if ((rc = grow(c->obidx, c->obidx_cap, bcap0, 0, c->stream))) return bail(rc);
+    if (cfg.edge_capacity > 0) {
+        if ((rc = grow(c->sbidx, c->sbidx_cap, bcap0, 0, c->stream))) return bail(rc);
+        if ((rc = grow(c->sbcost, c->sbcost_cap, bcap0, 0, c->stream))) return bail(rc);
+        if ((rc = grow(c->sobidx, c->sobidx_cap, bcap0, 0, c->stream))) return bail(rc);
+    }
     if ((rc = grow(c->app_bsum, c->app_bsum_cap, 2 * kAppendMaxBlocks + 2, 0, c->stream))) return bail(rc);
     for (int k = 0; k < 2; ++k)
         if ((rc = grow(c->odidx[k], c->odidx_cap[k], ecap0, 0, c->stream))) return bail(rc);
@@ -711,16 +719,19 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     int rc;
     if ((rc = set_device(c))) return rc;
     cudaStream_t s = c->stream;
-    // path_rev in path[0..n], its length in path[path_cap - 1]
-    int* len_dev = c->path + (c->path_cap - 1);
+    // one small read-back (header + the first kHead entries); a second copy
+    // only for paths longer than that
+    constexpr int kHead = 1020;
     const long long l0 = g_kernel_launches;
-    CU(launch_best_path(c->parent, c->n, c->path, len_dev, s));
+    CU(launch_best_path(c->parent, c->g, c->n, c->path, s));
     c->launches += g_kernel_launches - l0;
-    int len = 0;
-    double gg = 0.0;
-    CU(cudaMemcpyAsync(&len, len_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(&gg, c->g + kGoal, sizeof(double), cudaMemcpyDeviceToHost, s));
+    const int first = std::min<int64_t>(kHead, c->n + 1);
+    std::vector<int> buf(4 + first);
+    CU(cudaMemcpyAsync(buf.data(), c->path, sizeof(int) * (4 + first), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    const int len = buf[0];
+    double gg;
+    std::memcpy(&gg, &buf[2], sizeof(double));
     if (std::isinf(gg)) {
         if (len_out) *len_out = 0;
         if (cost_out) *cost_out = INFINITY;
@@ -728,8 +739,12 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     }
     if (len < 0) return fail(PIRRT_E_CORRUPT, "best_path: parent cycle");
     std::vector<int> rev(len);
-    CU(cudaMemcpyAsync(rev.data(), c->path, (size_t)len * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
+    std::copy(buf.begin() + 4, buf.begin() + 4 + std::min(len, first), rev.begin());
+    if (len > first) {
+        CU(cudaMemcpyAsync(rev.data() + first, c->path + 4 + first, (size_t)(len - first) * sizeof(int),
+                           cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    }
     if (len == 0 || rev.back() != kRoot)
         return fail(PIRRT_E_CORRUPT, "best_path: goal branch does not reach the root");
     if (cap < len) return fail(PIRRT_E_RANGE, "best_path: capacity too small");

@@ -182,7 +182,7 @@ cudaError_t launch_set_policy(const PolicyArgs& a, cudaStream_t s);
 cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* count_out,
                                  long long* cnt, long long* scan_tmp, cudaStream_t s);
 
-cudaError_t launch_best_path(const int* parent, int n, int* path_rev, int* len_out,
+cudaError_t launch_best_path(const int* parent, const double* g, int n, int* out,
                              cudaStream_t s);
 
 // device-wide exclusive scan: out[0..L] with out[L] = total

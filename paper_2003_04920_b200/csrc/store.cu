@@ -430,13 +430,15 @@ __global__ void k_check_policy(const int* parent_in, const double* g_in, int n, 
     if (err) atomicOr(&ctl->err, err);
 }
 
-__global__ void k_best_path(const int* parent, int n, int* path_rev, int* len_out) {
+// out[0] = length (-1: cycle), out[1..2] = g(goal) bits, out[4..] = goal..root
+__global__ void k_best_path(const int* parent, const double* g, int n, int* out) {
     int v = kGoal, len = 0;
     while (v != -1 && len <= n) {
-        path_rev[len++] = v;
+        out[4 + len++] = v;
         v = parent[v];
     }
-    *len_out = (v == -1) ? len : -1;   // -1: cycle
+    out[0] = (v == -1) ? len : -1;
+    *(double*)&out[2] = g[kGoal];
 }
 
 
@@ -875,10 +877,10 @@ cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* 
     return cudaGetLastError();
 }
 
-cudaError_t launch_best_path(const int* parent, int n, int* path_rev, int* len_out,
+cudaError_t launch_best_path(const int* parent, const double* g, int n, int* out,
                              cudaStream_t s) {
     ++g_kernel_launches;
-    k_best_path<<<1, 1, 0, s>>>(parent, n, path_rev, len_out);
+    k_best_path<<<1, 1, 0, s>>>(parent, g, n, out);
     return cudaGetLastError();
 }
 
