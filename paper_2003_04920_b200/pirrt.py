@@ -44,6 +44,8 @@ EXPORTS = (
     "pirrt_exploit", "pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
     "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
     "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id",
+    # include/pirrt_bench.h (measurement helpers)
+    "pirrt_bench_rows", "pirrt_bench_gather",
 )
 
 
@@ -111,6 +113,8 @@ def _load():
     lib.pirrt_kernel_launches.restype = C.c_int64
     lib.pirrt_last_error.restype = C.c_char_p
     lib.pirrt_nccl_unique_id.argtypes = [P, C.c_int64]
+    lib.pirrt_bench_rows.argtypes = [P, P, P, P, C.c_int32, C.c_int32, P]
+    lib.pirrt_bench_gather.argtypes = [P, P, C.c_int64, C.c_int32, P]
     return lib
 
 
@@ -133,6 +137,22 @@ pirrt_num_edges = _lib.pirrt_num_edges
 pirrt_kernel_launches = _lib.pirrt_kernel_launches
 pirrt_last_error = _lib.pirrt_last_error
 pirrt_nccl_unique_id = _lib.pirrt_nccl_unique_id
+
+
+def bench_rows(off, idx, cost, order, reps=5) -> float:
+    """ms per pass streaming CSR rows in `order` (torch CUDA tensors)."""
+    ms = C.c_float(0)
+    _check(_lib.pirrt_bench_rows(off.data_ptr(), idx.data_ptr(), cost.data_ptr(), order.data_ptr(),
+                                 int(order.numel()), int(reps), C.byref(ms)))
+    return float(ms.value)
+
+
+def bench_gather(src, idx, reps=5) -> float:
+    """ms per pass of idx.numel() random 8-byte gathers from src (torch CUDA tensors)."""
+    ms = C.c_float(0)
+    _check(_lib.pirrt_bench_gather(src.data_ptr(), idx.data_ptr(), int(idx.numel()), int(reps),
+                                   C.byref(ms)))
+    return float(ms.value)
 
 
 def nccl_unique_id() -> bytes:
