@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpirrt.so")
+LIB_PATH = os.environ.get("PIRRT_LIB") or os.path.join(_HERE, "lib", "libpirrt.so")
 
 PIRRT_OK = 0
 PIRRT_E_INVAL = -1
