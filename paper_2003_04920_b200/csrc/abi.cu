@@ -154,6 +154,10 @@ struct pirrt_ctx {
     unsigned* stamp = nullptr; int64_t stamp_cap = 0;
     int* Bq[2] = {nullptr, nullptr}; int64_t Bq_cap[2] = {0, 0};
     int* qdepth = nullptr; int64_t qdepth_cap = 0;
+    char* slab = nullptr; size_t slab_bytes = 0;          // hot per-vertex arrays (one allocation)
+    bool l2_persist = true;                              // PIRRT_L2_PERSIST=0 disables
+    int64_t persist_max = 0, window_max = 0;
+    L2Window l2win;
     int Bsel = 0;
     int Bcount = 0;
     unsigned ev_next = 1;
@@ -199,6 +203,64 @@ int set_device(const pirrt_ctx* c) {
     return 0;
 }
 
+// The per-vertex arrays every PI phase gathers from (g, pc, h, parent, stamp,
+// b and the two B lists) live in ONE allocation, so a single L2 access-policy
+// window can keep them resident (persisting lines survive other traffic, e.g.
+// the benchmark's L2 flush).  Growth copies each sub-array.
+int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
+    cudaStream_t s = c->stream;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t sz_g = al(8 * cap), sz_pc = al(8 * cap), sz_h = al(8 * cap);
+    const size_t sz_par = al(4 * cap), sz_st = al(4 * cap), sz_bq = al(4 * (cap + 2)), sz_b = al(cap);
+    const size_t total = sz_g + sz_pc + sz_h + sz_par + sz_st + 2 * sz_bq + sz_b;
+    char* slab = nullptr;
+    if (cudaMalloc(&slab, total) != cudaSuccess) { cudaGetLastError(); return fail(PIRRT_E_NOMEM, "cudaMalloc (vertex slab) failed"); }
+    char* q = slab;
+    double* g = (double*)q; q += sz_g;
+    double* pc = (double*)q; q += sz_pc;
+    double* h = (double*)q; q += sz_h;
+    int* parent = (int*)q; q += sz_par;
+    unsigned* stamp = (unsigned*)q; q += sz_st;
+    int* bq0 = (int*)q; q += sz_bq;
+    int* bq1 = (int*)q; q += sz_bq;
+    unsigned char* b = (unsigned char*)q;
+    const int64_t n = c->n;
+    // stamps of fresh slots read as "never visited"; list slots beyond the
+    // live entries are -1 (work-queue invariant), slot 0 = root
+    CU(cudaMemsetAsync(stamp, 0, (size_t)cap * sizeof(unsigned), s));
+    CU(cudaMemsetAsync(bq0, 0xFF, (size_t)(cap + 2) * sizeof(int), s));
+    CU(cudaMemsetAsync(bq1, 0xFF, (size_t)(cap + 2) * sizeof(int), s));
+    CU(cudaMemsetAsync(bq0, 0, sizeof(int), s));
+    CU(cudaMemsetAsync(bq1, 0, sizeof(int), s));
+    if (c->slab) {
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s) : cudaSuccess;
+        };
+        int* nbq[2] = {bq0, bq1};
+        const int64_t keep_cur = 1 + c->Bcount;
+        if (cp(g, c->g, 8 * n) || cp(pc, c->pc, 8 * n) || cp(h, c->h, 8 * n) ||
+            cp(parent, c->parent, 4 * n) || cp(stamp, c->stamp, 4 * n) || cp(b, c->b, n) ||
+            cp(nbq[c->Bsel], c->Bq[c->Bsel], 4 * keep_cur))
+            return fail(PIRRT_E_CUDA, "vertex slab copy failed");
+        CU(cudaStreamSynchronize(s));
+        CU(cudaFree(c->slab));
+    }
+    c->slab = slab; c->slab_bytes = total;
+    c->g = g; c->pc = pc; c->h = h; c->parent = parent; c->stamp = stamp; c->b = b;
+    c->Bq[0] = bq0; c->Bq[1] = bq1; c->Bq_cap[0] = c->Bq_cap[1] = cap + 2;
+    c->g_cap = c->pc_cap = c->h_cap = c->parent_cap = c->b_cap = c->stamp_cap = cap;
+    // L2 persistence for the slab
+    if (c->l2_persist) {
+        size_t lim = std::min<size_t>(total, (size_t)c->persist_max);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+        c->l2win.base = slab;
+        c->l2win.bytes = std::min<size_t>(total, (size_t)c->window_max);
+        c->l2win.hit = c->l2win.bytes ? std::min(1.0f, (float)lim / (float)c->l2win.bytes) : 0.f;
+        cudaGetLastError();
+    }
+    return 0;
+}
+
 // make every per-vertex array hold at least `need` vertices (+1 for offsets)
 int ensure_vertices(pirrt_ctx* c, int64_t need) {
     if (need <= c->vcap) return 0;
@@ -207,11 +269,7 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
     const int64_t n = c->n;
     cudaStream_t s = c->stream;
     int rc;
-    if ((rc = grow(c->g, c->g_cap, cap, n, s))) return rc;
-    if ((rc = grow(c->h, c->h_cap, cap, n, s))) return rc;
-    if ((rc = grow(c->pc, c->pc_cap, cap, n, s))) return rc;
-    if ((rc = grow(c->parent, c->parent_cap, cap, n, s))) return rc;
-    if ((rc = grow(c->b, c->b_cap, cap, n, s))) return rc;
+    if ((rc = grow_hot_slab(c, cap))) return rc;
     if ((rc = grow(c->boff, c->boff_cap, cap + 1, n + 1, s))) return rc;
     if ((rc = grow(c->sboff, c->sboff_cap, cap + 1, 0, s))) return rc;
     if ((rc = grow(c->doff[c->cur], c->doff_cap[c->cur], cap + 1, n + 1, s))) return rc;
@@ -222,22 +280,6 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
     if ((rc = grow(c->soboff, c->soboff_cap, cap + 1, 0, s))) return rc;
     if ((rc = grow(c->odoff[c->cur], c->odoff_cap[c->cur], cap + 1, n + 1, s))) return rc;
     if ((rc = grow(c->odoff[1 - c->cur], c->odoff_cap[1 - c->cur], cap + 1, 0, s))) return rc;
-    {
-        const int64_t old_cap = c->stamp_cap;
-        if ((rc = grow(c->stamp, c->stamp_cap, cap, n, s))) return rc;
-        if (c->stamp_cap > old_cap)   // fresh slots must read as "never visited"
-            CU(cudaMemsetAsync(c->stamp + n, 0, (size_t)(c->stamp_cap - n) * sizeof(unsigned), s));
-    }
-    for (int k = 0; k < 2; ++k) {
-        // list buffers: slots beyond the live entries are -1 (work-queue invariant)
-        const int64_t keep = (k == c->Bsel) ? 1 + c->Bcount : 1;
-        const int64_t old_cap = c->Bq_cap[k];
-        if ((rc = grow(c->Bq[k], c->Bq_cap[k], cap + 2, keep, s))) return rc;
-        if (c->Bq_cap[k] != old_cap) {
-            CU(cudaMemsetAsync(c->Bq[k] + keep, 0xFF, (size_t)(c->Bq_cap[k] - keep) * sizeof(int), s));
-            if (old_cap == 0) CU(cudaMemsetAsync(c->Bq[k], 0, sizeof(int), s));   // slot 0 = root
-        }
-    }
     if ((rc = grow(c->qdepth, c->qdepth_cap, cap + 2, 0, s))) return rc;
     if ((rc = grow(c->path, c->path_cap, cap + 8, 0, s))) return rc;
     c->vcap = cap;
@@ -245,11 +287,11 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
 }
 
 void free_all(pirrt_ctx* c) {
-    void* ptrs[] = {c->g, c->h, c->pc, c->parent, c->b, c->boff, c->bidx, c->bcost,
+    void* ptrs[] = {c->slab, c->boff, c->bidx, c->bcost,
                     c->sboff, c->sbidx, c->sbcost, c->soboff, c->sobidx,
                     c->doff[0], c->doff[1], c->didx[0], c->didx[1], c->dcost[0], c->dcost[1],
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
-                    c->stamp, c->Bq[0], c->Bq[1], c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
+                    c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
                     c->rec_local, c->rec_all, c->rec_counts, c->app_bsum};
     for (void* p : ptrs)
@@ -374,6 +416,10 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (cudaGetDeviceProperties(&prop, cfg.device) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "create: device properties"));
     c->num_sms = prop.multiProcessorCount;
+    c->persist_max = prop.persistingL2CacheMaxSize;
+    c->window_max = prop.accessPolicyMaxWindowSize;
+    if (const char* w = std::getenv("PIRRT_L2_PERSIST")) c->l2_persist = std::atoi(w) != 0;
+    if (c->persist_max <= 0 || c->window_max <= 0) c->l2_persist = false;
     if (!prop.cooperativeLaunch) return bail(fail(PIRRT_E_STATE, "create: no cooperative launch"));
     int per_sm = exploit_blocks_per_sm();
     if (per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: exploit kernel does not fit an SM"));
@@ -517,7 +563,7 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     a.grid_blocks = c->num_sms;
     const long long l0 = g_kernel_launches;
     cudaError_t e = c->fused_append
-        ? launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks, s)
+        ? launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks, c->l2win, s)
         : launch_append(a, s);
     c->launches += g_kernel_launches - l0;
     if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("append: ") + cudaGetErrorString(e)); }
@@ -639,7 +685,7 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
         ExploitArgs a;
         fill_exploit_args(c, a);
         const long long l0 = g_kernel_launches;
-        cudaError_t e = launch_exploit(a, c->grid_blocks, s);
+        cudaError_t e = launch_exploit(a, c->grid_blocks, c->l2win, s);
         c->launches += g_kernel_launches - l0;
         if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
         CU(cudaEventRecord(c->ev1, s));

@@ -114,8 +114,19 @@ struct ExploitArgs {
 // delta of each call to its context)
 extern thread_local long long g_kernel_launches;
 
+// L2 access-policy window (persisting) for the hot vertex slab; bytes == 0: none
+struct L2Window {
+    void* base = nullptr;
+    size_t bytes = 0;
+    float hit = 0.f;
+};
+
+// cudaLaunchKernelEx helper: cooperative launch + optional persisting window
+cudaError_t launch_coop(const void* fn, int blocks, int threads, void** params,
+                        const L2Window& w, cudaStream_t s);
+
 // ---- launchers (store.cu / exploit.cu) ----
-cudaError_t launch_exploit(const ExploitArgs& a, int blocks, cudaStream_t s);
+cudaError_t launch_exploit(const ExploitArgs& a, int blocks, const L2Window& w, cudaStream_t s);
 cudaError_t launch_shard_improve(const ExploitArgs& a, int it, int blocks, cudaStream_t s);
 cudaError_t launch_shard_evaluate(const ExploitArgs& a, int it, const ShardRec* recs,
                                   const int* counts, int stride, int nranks, int blocks,
@@ -156,7 +167,7 @@ struct AppendArgs {
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t s);
 // one cooperative kernel for the whole append; bsum needs 2 * max_blocks entries
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
-                                int max_blocks, cudaStream_t s);
+                                int max_blocks, const L2Window& w, cudaStream_t s);
 constexpr int kAppendMaxBlocks = 2048;
 
 // fold a delta CSR into its base CSR (cost arrays may be NULL: out-index)

@@ -831,7 +831,7 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
-                                int max_blocks, cudaStream_t s) {
+                                int max_blocks, const L2Window& w, cudaStream_t s) {
     static int per_sm = -1;
     if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_append_fused, kBT, 0);
     int blocks = per_sm * (a.grid_blocks > 0 ? a.grid_blocks : 148);
@@ -840,8 +840,7 @@ cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long*
     AppendArgs args = a;
     void* params[] = {&args, &cnt1, &bsum};
     ++g_kernel_launches;
-    return cudaLaunchCooperativeKernel((const void*)k_append_fused, dim3(blocks), dim3(kBT), params,
-                                       0, s);
+    return launch_coop((const void*)k_append_fused, blocks, kBT, params, w, s);
 }
 
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
