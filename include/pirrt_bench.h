@@ -17,6 +17,11 @@ extern "C" {
 int pirrt_bench_rows(const long long* off, const int* idx, const double* cost, const int* order,
                      int32_t nrows, int32_t reps, float* ms_out);
 
+/* One relaxation pass: rows in `order` (warp per row), out[v] = min over the
+ * row of cost + g[idx] -- 12 B streamed + one 8 B gather per entry. */
+int pirrt_bench_relax(const long long* off, const int* idx, const double* cost, const double* g,
+                      const int* order, int32_t nrows, double* out, int32_t reps, float* ms_out);
+
 /* n random 8-byte gathers src[idx[i]] (idx streamed): 4 B + one 8 B gather each. */
 int pirrt_bench_gather(const double* src, const int* idx, int64_t n, int32_t reps, float* ms_out);
 

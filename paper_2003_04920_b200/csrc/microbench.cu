@@ -26,6 +26,27 @@ __global__ void k_rows(const long long* __restrict__ off, const int* __restrict_
     if (acc == -1.0) *sink = acc;   // keep the loads alive
 }
 
+// rows + g[u] gathers + a min per row (what one relaxation pass costs when
+// nothing else happens): 20 B algorithmic per entry
+__global__ void k_relax(const long long* __restrict__ off, const int* __restrict__ idx,
+                        const double* __restrict__ cost, const double* __restrict__ g,
+                        const int* __restrict__ order, int nrows, double* out) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = w; r < nrows; r += nw) {
+        const int v = order[r];
+        const long long k0 = __ldg(&off[v]), k1 = __ldg(&off[v + 1]);
+        double best = 1e300;
+        for (long long k = k0 + lane; k < k1; k += 32) {
+            const double cand = __ldg(&cost[k]) + __ldcg(&g[__ldg(&idx[k])]);
+            best = cand < best ? cand : best;
+        }
+        for (int o = 16; o; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) out[v] = best;
+    }
+}
+
 __global__ void k_gather(const double* __restrict__ src, const int* __restrict__ idx, long long n,
                          double* sink) {
     double acc = 0.0;
@@ -52,6 +73,7 @@ float time_it(void (*launch)(void*), void* arg, int reps) {
 }
 
 struct RowsArg { const long long* off; const int* idx; const double* cost; const int* order; int n; double* sink; int blocks; };
+struct RelaxArg { const long long* off; const int* idx; const double* cost; const double* g; const int* order; int n; double* out; int blocks; };
 struct GatherArg { const double* src; const int* idx; long long n; double* sink; int blocks; };
 
 }  // namespace
@@ -70,6 +92,18 @@ int pirrt_bench_rows(const long long* off, const int* idx, const double* cost, c
         k_rows<<<r->blocks, 256>>>(r->off, r->idx, r->cost, r->order, r->n, r->sink);
     }, &a, reps);
     cudaFree(sink);
+    return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+int pirrt_bench_relax(const long long* off, const int* idx, const double* cost, const double* g,
+                      const int* order, int32_t nrows, double* out, int32_t reps, float* ms_out) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    RelaxArg a{off, idx, cost, g, order, nrows, out, sms * 8};
+    *ms_out = time_it([](void* p) {
+        RelaxArg* r = (RelaxArg*)p;
+        k_relax<<<r->blocks, 256>>>(r->off, r->idx, r->cost, r->g, r->order, r->n, r->out);
+    }, &a, reps);
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 

@@ -45,7 +45,7 @@ EXPORTS = (
     "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
     "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id",
     # include/pirrt_bench.h (measurement helpers)
-    "pirrt_bench_rows", "pirrt_bench_gather",
+    "pirrt_bench_rows", "pirrt_bench_relax", "pirrt_bench_gather",
 )
 
 
@@ -115,6 +115,7 @@ def _load():
     lib.pirrt_nccl_unique_id.argtypes = [P, C.c_int64]
     lib.pirrt_bench_rows.argtypes = [P, P, P, P, C.c_int32, C.c_int32, P]
     lib.pirrt_bench_gather.argtypes = [P, P, C.c_int64, C.c_int32, P]
+    lib.pirrt_bench_relax.argtypes = [P, P, P, P, P, C.c_int32, P, C.c_int32, P]
     return lib
 
 
@@ -144,6 +145,15 @@ def bench_rows(off, idx, cost, order, reps=5) -> float:
     ms = C.c_float(0)
     _check(_lib.pirrt_bench_rows(off.data_ptr(), idx.data_ptr(), cost.data_ptr(), order.data_ptr(),
                                  int(order.numel()), int(reps), C.byref(ms)))
+    return float(ms.value)
+
+
+def bench_relax(off, idx, cost, g, order, out, reps=5) -> float:
+    """ms per relaxation pass over the rows in `order` (torch CUDA tensors)."""
+    ms = C.c_float(0)
+    _check(_lib.pirrt_bench_relax(off.data_ptr(), idx.data_ptr(), cost.data_ptr(), g.data_ptr(),
+                                  order.data_ptr(), int(order.numel()), out.data_ptr(), int(reps),
+                                  C.byref(ms)))
     return float(ms.value)
 
 

@@ -50,16 +50,20 @@ def test_struct_layouts_match_header():
 
 
 def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    # a fresh import with the library path pointing at nothing must raise,
+    # never fall back to anything
     import importlib.util
+    import sys
+    monkeypatch.setenv("PIRRT_LIB", str(tmp_path / "libpirrt.so"))
     spec = importlib.util.spec_from_file_location(
-        "pirrt_copy", os.path.join(ROOT, "paper_2003_04920_b200", "pirrt.py"))
+        "pirrt_missing_copy", os.path.join(ROOT, "paper_2003_04920_b200", "pirrt.py"))
     mod = importlib.util.module_from_spec(spec)
-    # point the copy at an empty directory: import must raise, not fall back
-    src = open(spec.origin).read().replace(
-        'LIB_PATH = os.path.join(_HERE, "lib", "libpirrt.so")',
-        f'LIB_PATH = {str(tmp_path / "libpirrt.so")!r}')
-    with pytest.raises(ImportError):
-        exec(compile(src, spec.origin, "exec"), mod.__dict__)
+    sys.modules["pirrt_missing_copy"] = mod
+    try:
+        with pytest.raises(ImportError):
+            spec.loader.exec_module(mod)
+    finally:
+        sys.modules.pop("pirrt_missing_copy", None)
 
 
 def test_so_is_sm100a():

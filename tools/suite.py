@@ -125,6 +125,11 @@ def microbench(g):
     E = int(off[-1])
     ms_rows = pirrt.bench_rows(t_off, t_idx, t_cost, rows, reps=10)
     res = {"rows_stream": {"edges": E, "ms": ms_rows, "GBps": 12 * E / (ms_rows * 1e-3) / 1e9}}
+    gvec = torch.rand(n, dtype=torch.float64, device="cuda")
+    outv = torch.empty(n, dtype=torch.float64, device="cuda")
+    ms_rel = pirrt.bench_relax(t_off, t_idx, t_cost, gvec, rows, outv, reps=10)
+    res["relax_pass"] = {"edges": E, "ms": ms_rel, "GBps_algorithmic": 20 * E / (ms_rel * 1e-3) / 1e9,
+                         "G_relax_per_s": E / (ms_rel * 1e-3) / 1e9}
     for name, arr_n in (("gather_L2_8MB", 1_000_000), ("gather_HBM_2GB", 256_000_000)):
         src_arr = torch.rand(arr_n, dtype=torch.float64, device="cuda")
         idx = torch.randint(0, arr_n, (64_000_000,), dtype=torch.int32, device="cuda")
