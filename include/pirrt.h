@@ -63,7 +63,8 @@ enum {
 };
 
 typedef struct {
-    int64_t vertex_capacity;  /* initial reservation (hint; the store grows past it)        */
+    int64_t vertex_capacity;  /* initial reservation (hint; grows up to 2^30 - 2^14 vertices,
+                                 beyond which append returns PIRRT_E_RANGE)                 */
     int64_t edge_capacity;    /* initial directed-edge reservation (hint)                    */
     double h_root;            /* h(x_init); default 0                                       */
     double h_goal;            /* h(x_goal); default 0                                       */

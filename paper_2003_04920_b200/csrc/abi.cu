@@ -153,7 +153,8 @@ struct pirrt_ctx {
     // Evaluate stamps and the B lists (entry 0 = root)
     unsigned* stamp = nullptr; int64_t stamp_cap = 0;
     int* Bq[2] = {nullptr, nullptr}; int64_t Bq_cap[2] = {0, 0};
-    int* qdepth = nullptr; int64_t qdepth_cap = 0;
+    // work-queue Evaluate items (slot 0 = root, the rest -1 between Evaluates)
+    int* qv = nullptr; double* qg = nullptr; int* qdepth = nullptr; int64_t q_cap = 0;
     char* slab = nullptr; size_t slab_bytes = 0;          // hot per-vertex arrays (one allocation)
     bool l2_persist = true;                              // PIRRT_L2_PERSIST=0 disables
     int64_t persist_max = 0, window_max = 0;
@@ -189,9 +190,11 @@ struct pirrt_ctx {
     int shard_blocks = 0;
     unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
     double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
-    int bfs_async = 0;
+    int bfs_wq = 0;                                          // PIRRT_BFS=wq: work-queue Evaluate (experimental)
+    int halves = 4;                                          // PIRRT_HALVES: 16-lane items above halves * warps
+    int wq_keep = 32;                                        // PIRRT_WQ_KEEP
     int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
-    long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;                                       // PIRRT_BFS=async: barrier-free work-queue Evaluate (experimental)
+    long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
 };
 
@@ -264,8 +267,10 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
 // make every per-vertex array hold at least `need` vertices (+1 for offsets)
 int ensure_vertices(pirrt_ctx* c, int64_t need) {
     if (need <= c->vcap) return 0;
+    // vertex ids travel as (id << 1 | tag) inside the Evaluate scan
+    if (need > kMaxVertices) return fail(PIRRT_E_RANGE, "more than 2^30 - 2^14 vertices");
     int64_t cap = std::max<int64_t>(need, c->vcap + c->vcap / 2);
-    cap = std::max<int64_t>(cap, 1024);
+    cap = std::min<int64_t>(std::max<int64_t>(cap, 1024), kMaxVertices);
     const int64_t n = c->n;
     cudaStream_t s = c->stream;
     int rc;
@@ -280,7 +285,21 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
     if ((rc = grow(c->soboff, c->soboff_cap, cap + 1, 0, s))) return rc;
     if ((rc = grow(c->odoff[c->cur], c->odoff_cap[c->cur], cap + 1, n + 1, s))) return rc;
     if ((rc = grow(c->odoff[1 - c->cur], c->odoff_cap[1 - c->cur], cap + 1, 0, s))) return rc;
-    if ((rc = grow(c->qdepth, c->qdepth_cap, cap + 2, 0, s))) return rc;
+    if (cap + 2 + kMaxGridBlocks > c->q_cap) {
+        // fresh queue: every slot unpublished (-1) except slot 0 = the root (g 0, depth 0)
+        const int64_t qc = cap + 2 + kMaxGridBlocks;
+        int64_t c1 = 0, c2 = 0, c3 = 0;
+        if (c->qv) { CU(cudaStreamSynchronize(s)); cudaFree(c->qv); cudaFree(c->qg); cudaFree(c->qdepth); }
+        c->qv = nullptr; c->qg = nullptr; c->qdepth = nullptr;
+        if ((rc = grow(c->qv, c1, qc, 0, s))) return rc;
+        if ((rc = grow(c->qg, c2, qc, 0, s))) return rc;
+        if ((rc = grow(c->qdepth, c3, qc, 0, s))) return rc;
+        CU(cudaMemsetAsync(c->qv, 0xff, (size_t)qc * sizeof(int), s));
+        CU(cudaMemsetAsync(c->qv, 0, sizeof(int), s));
+        CU(cudaMemsetAsync(c->qg, 0, (size_t)qc * sizeof(double), s));
+        CU(cudaMemsetAsync(c->qdepth, 0, (size_t)qc * sizeof(int), s));
+        c->q_cap = qc;
+    }
     if ((rc = grow(c->path, c->path_cap, cap + 8, 0, s))) return rc;
     c->vcap = cap;
     return 0;
@@ -291,7 +310,7 @@ void free_all(pirrt_ctx* c) {
                     c->sboff, c->sbidx, c->sbcost, c->soboff, c->sobidx,
                     c->doff[0], c->doff[1], c->didx[0], c->didx[1], c->dcost[0], c->dcost[1],
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
-                    c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
+                    c->qv, c->qg, c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
                     c->rec_local, c->rec_all, c->rec_counts, c->app_bsum};
     for (void* p : ptrs)
@@ -402,7 +421,9 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_WATCHDOG_MS"))
         c->watchdog_ns = (unsigned long long)std::strtoull(w, nullptr, 10) * 1000000ull;
     if (const char* w = std::getenv("PIRRT_COMPACT_MIN")) c->compact_min = std::atof(w);
-    if (const char* w = std::getenv("PIRRT_BFS")) c->bfs_async = std::strcmp(w, "async") == 0;
+    if (const char* w = std::getenv("PIRRT_BFS")) c->bfs_wq = std::strcmp(w, "wq") == 0;
+    if (const char* w = std::getenv("PIRRT_HALVES")) c->halves = std::max(1, std::atoi(w));
+    if (const char* w = std::getenv("PIRRT_WQ_KEEP")) c->wq_keep = std::max(1, std::min(64, std::atoi(w)));
     if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
@@ -425,6 +446,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: exploit kernel does not fit an SM"));
     c->grid_blocks = cfg.grid_blocks > 0 ? std::min(cfg.grid_blocks, per_sm * c->num_sms)
                                          : per_sm * c->num_sms;
+    c->grid_blocks = std::min(c->grid_blocks, kMaxGridBlocks);
     int rc;
     int64_t vcap0 = std::max<int64_t>(cfg.vertex_capacity, 1024);
     if ((rc = ensure_vertices(c, vcap0))) return bail(rc);
@@ -467,6 +489,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         if (per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: shard kernel does not fit an SM"));
         c->shard_blocks = cfg.grid_blocks > 0 ? std::min(cfg.grid_blocks, per_sm * c->num_sms)
                                               : per_sm * c->num_sms;
+        c->shard_blocks = std::min(c->shard_blocks, kMaxGridBlocks);
         if ((rc = grow(c->rec_counts, c->rec_counts_cap, cfg.nranks + 1, 0, c->stream))) return bail(rc);
     }
     // V = {x_init, x_goal}, E = {}, B = {}
@@ -600,9 +623,11 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.eps = c->cfg.epsilon;
     a.prune_off = (c->cfg.flags & PIRRT_F_PRUNE_OFF) ? 1 : 0;
     a.watchdog_ns = c->watchdog_ns;
-    a.bfs_async = c->bfs_async;
+    a.bfs_wq = c->bfs_wq;
+    a.wq_keep = c->wq_keep;
+    a.halves = c->halves;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
-    a.qdepth = c->qdepth;
+    a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;
 }
 
 // Sharded exploit: per PI iteration

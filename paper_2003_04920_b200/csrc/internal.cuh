@@ -12,6 +12,8 @@ namespace pirrt {
 constexpr int kRoot = 0;          // x_init
 constexpr int kGoal = 1;          // x_goal
 constexpr int kThreads = 512;     // persistent-kernel block size
+constexpr int kMaxGridBlocks = 8192;  // queue slack: claims beyond the last published slot
+constexpr long long kMaxVertices = (1LL << 30) - (1LL << 14);
 constexpr unsigned kFull = 0xffffffffu;
 
 // validation error bits (append / set_policy)
@@ -32,9 +34,12 @@ struct IterCtl {
     int g_changed;                // some g bit changed in Evaluate
     int both;                     // |old B  n  new B|
     int lpush[3];                 // expanded vertices per BFS level (rotating slots)
-    int qpushed;                  // async BFS: items pushed after the root
-    int qdone;                    // async BFS: items processed (flushed lazily)
     int lvis[3];                  // "some child visited" per BFS level (rotating slots)
+    // work-queue Evaluate: queue slot 0 holds the root permanently
+    int qhead;                    // slots claimed by blocks
+    int qtail;                    // slots published after the root
+    int qout;                     // published-but-unfinished items, minus 1 (root): -1 = done
+    int bcnt;                     // entries written to the new B list
 };
 
 // One Improve result in sharded mode (all-gathered between ranks).
@@ -59,6 +64,7 @@ struct DevCtl {
     long long relaxations, eval_visits, improve_set, eval_scanned;
     unsigned long long t_improve, t_evaluate;
     unsigned long long dbg_work_ns;   // PIRRT_DEBUG level trace
+    unsigned long long dbg[8];        // PIRRT_LEVEL_TRACE work-queue counters
     // append / set_policy
     int err;                      // bitmask of kErr*
     int nprom;                    // new promising vertices
@@ -88,7 +94,10 @@ struct ExploitArgs {
     double* pc;
     unsigned char* b;
     unsigned* stamp;              // 2e: visited in Evaluate e; 2e+1: expanded in e
-    int* qdepth;                  // async BFS: depth of the vertex in queue slot i
+    // work-queue Evaluate: item of queue slot i (qv[i] == -1: not yet published)
+    int* qv;
+    double* qg;
+    int* qdepth;
     // B lists (entry 0 = root, B = [1, 1 + count)); Bq[Bsel] is current
     int* Bq0;
     int* Bq1;
@@ -106,7 +115,9 @@ struct ExploitArgs {
     double eps;
     int prune_off;
     unsigned long long watchdog_ns;   // abort the loop after this long (diagnostic guard)
-    int bfs_async;                    // 1: barrier-free work-queue Evaluate, 0: level-synchronous
+    int bfs_wq;                       // 1: work-queue Evaluate, 0: level-synchronous
+    int halves;                       // level-synchronous: 16 lanes per vertex above halves * warps
+    int wq_keep;                      // work-queue Evaluate: items a block keeps per local level
     int debug;                        // PIRRT_DEBUG: device diagnostics
 };
 

@@ -257,7 +257,7 @@ def test_noconv_cap(P):
     assert ei.value.code == P.PIRRT_E_NOCONV
 
 
-# ------------------------------------------------------------------ sharded / async paths
+# ------------------------------------------------------------------ sharded / Evaluate variants
 
 @pytest.mark.parametrize("flags", [0, PRUNE_OFF])
 def test_sharded_loop_single_rank_parity(P, flags):
@@ -276,13 +276,32 @@ def test_sharded_loop_6d(P):
     dual_replay(gpu, orc, r, 1000)
 
 
-def test_async_evaluate_parity(P, monkeypatch):
-    # the barrier-free work-queue Evaluate (PIRRT_BFS=async) must agree too
-    monkeypatch.setenv("PIRRT_BFS", "async")
+@pytest.mark.parametrize("bfs,keep,halves", [("level", None, "1"), ("wq", "1", None),
+                                             ("wq", "7", None), ("wq", "64", None)])
+def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves):
+    # both Evaluate variants (level-synchronous, here with 16-lane items from
+    # small frontiers on; work queue, whose local frontier size wq_keep
+    # decides how much goes through the global queue) must agree with the oracle
+    monkeypatch.setenv("PIRRT_BFS", bfs)
+    if keep:
+        monkeypatch.setenv("PIRRT_WQ_KEEP", keep)
+    if halves:
+        monkeypatch.setenv("PIRRT_HALVES", halves)
     r = gen.rrg(2, 4000, gen.gamma_star(2), n_boxes=25, seed=gen.seed_of("async"))
     gpu = P.Context(h_root=r.h_root())
     orc = Oracle(h_root=r.h_root())
     dual_replay(gpu, orc, r, 50)
+
+
+@pytest.mark.parametrize("gb", [1, 2, 5])
+def test_work_queue_small_grids_6d(P, monkeypatch, gb):
+    # few blocks: claims run far ahead of publication, staging overflows
+    monkeypatch.setenv("PIRRT_BFS", "wq")
+    monkeypatch.setenv("PIRRT_WQ_KEEP", "3")
+    r = gen.rrg(6, 8000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("wq-small", gb))
+    gpu = P.Context(h_root=r.h_root(), grid_blocks=gb)
+    orc = Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, 700)
 
 
 def test_split_append_path_parity(P, monkeypatch):
