@@ -191,8 +191,10 @@ struct pirrt_ctx {
     unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
     double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
     int bfs_wq = 0;                                          // PIRRT_BFS=wq: work-queue Evaluate (experimental)
-    int halves = 4;                                          // PIRRT_HALVES: 16-lane items above halves * warps
+    int halves = 0;                                          // PIRRT_HALVES=k: warp-per-item levels (16 lanes
+                                                             // above k * warps); 0: block-chunked edge-parallel
     int wq_keep = 32;                                        // PIRRT_WQ_KEEP
+    int wq_tail = -1;                                        // PIRRT_WQ_TAIL (-1: 16 per block)
     int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
@@ -422,8 +424,9 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         c->watchdog_ns = (unsigned long long)std::strtoull(w, nullptr, 10) * 1000000ull;
     if (const char* w = std::getenv("PIRRT_COMPACT_MIN")) c->compact_min = std::atof(w);
     if (const char* w = std::getenv("PIRRT_BFS")) c->bfs_wq = std::strcmp(w, "wq") == 0;
-    if (const char* w = std::getenv("PIRRT_HALVES")) c->halves = std::max(1, std::atoi(w));
+    if (const char* w = std::getenv("PIRRT_HALVES")) c->halves = std::max(0, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_WQ_KEEP")) c->wq_keep = std::max(1, std::min(64, std::atoi(w)));
+    if (const char* w = std::getenv("PIRRT_WQ_TAIL")) c->wq_tail = std::atoi(w);
     if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
@@ -625,6 +628,8 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.watchdog_ns = c->watchdog_ns;
     a.bfs_wq = c->bfs_wq;
     a.wq_keep = c->wq_keep;
+    // the hand-over frontier must fit the blocks' local frontiers (64 each)
+    a.wq_tail = c->wq_tail < 0 ? 16 * c->grid_blocks : std::min(c->wq_tail, 64 * c->grid_blocks);
     a.halves = c->halves;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
     a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;

@@ -11,7 +11,10 @@ namespace pirrt {
 
 constexpr int kRoot = 0;          // x_init
 constexpr int kGoal = 1;          // x_goal
-constexpr int kThreads = 512;     // persistent-kernel block size
+#ifndef PIRRT_THREADS
+#define PIRRT_THREADS 512
+#endif
+constexpr int kThreads = PIRRT_THREADS;   // persistent-kernel block size
 constexpr int kMaxGridBlocks = 8192;  // queue slack: claims beyond the last published slot
 constexpr long long kMaxVertices = (1LL << 30) - (1LL << 14);
 constexpr unsigned kFull = 0xffffffffu;
@@ -37,8 +40,8 @@ struct IterCtl {
     int lvis[3];                  // "some child visited" per BFS level (rotating slots)
     // work-queue Evaluate: queue slot 0 holds the root permanently
     int qhead;                    // slots claimed by blocks
-    int qtail;                    // slots published after the root
-    int qout;                     // published-but-unfinished items, minus 1 (root): -1 = done
+    int qtail;                    // slots reserved by publishers
+    int qout;                     // (children created - items expanded): -F0 = done
     int bcnt;                     // entries written to the new B list
 };
 
@@ -65,6 +68,9 @@ struct DevCtl {
     unsigned long long t_improve, t_evaluate;
     unsigned long long dbg_work_ns;   // PIRRT_DEBUG level trace
     unsigned long long dbg[8];        // PIRRT_LEVEL_TRACE work-queue counters
+    unsigned long long dbg_imp[6];    // PIRRT_LEVEL_TRACE Improve timeline
+    unsigned long long dbg_lv[32][6]; // PIRRT_LEVEL_TRACE per level: ~min start, max start,
+                                      // max work end, max flush end, lead exit, frontier
     // append / set_policy
     int err;                      // bitmask of kErr*
     int nprom;                    // new promising vertices
@@ -118,6 +124,8 @@ struct ExploitArgs {
     int bfs_wq;                       // 1: work-queue Evaluate, 0: level-synchronous
     int halves;                       // level-synchronous: 16 lanes per vertex above halves * warps
     int wq_keep;                      // work-queue Evaluate: items a block keeps per local level
+    int wq_tail;                      // level-synchronous: hand a shrinking frontier of at most
+                                      // this many items to the work queue (0: never)
     int debug;                        // PIRRT_DEBUG: device diagnostics
 };
 

@@ -276,17 +276,24 @@ def test_sharded_loop_6d(P):
     dual_replay(gpu, orc, r, 1000)
 
 
-@pytest.mark.parametrize("bfs,keep,halves", [("level", None, "1"), ("wq", "1", None),
-                                             ("wq", "7", None), ("wq", "64", None)])
-def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves):
-    # both Evaluate variants (level-synchronous, here with 16-lane items from
-    # small frontiers on; work queue, whose local frontier size wq_keep
-    # decides how much goes through the global queue) must agree with the oracle
+@pytest.mark.parametrize("bfs,keep,halves,tail", [("level", None, "1", "0"), ("level", None, "4", None),
+                                                  ("level", "2", None, "100000"),
+                                                  ("level", None, None, "0"),
+                                                  ("wq", "1", None, None), ("wq", "7", None, None),
+                                                  ("wq", "64", None, None)])
+def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves, tail):
+    # the Evaluate variants must agree with the oracle: level-synchronous
+    # (block-chunked or one warp per item, 16-lane items from small frontiers
+    # on, with or without handing the shrinking tail to the work queue), and
+    # the work queue from the root (its local frontier size wq_keep decides
+    # how much goes through the global queue)
     monkeypatch.setenv("PIRRT_BFS", bfs)
     if keep:
         monkeypatch.setenv("PIRRT_WQ_KEEP", keep)
     if halves:
         monkeypatch.setenv("PIRRT_HALVES", halves)
+    if tail:
+        monkeypatch.setenv("PIRRT_WQ_TAIL", tail)
     r = gen.rrg(2, 4000, gen.gamma_star(2), n_boxes=25, seed=gen.seed_of("async"))
     gpu = P.Context(h_root=r.h_root())
     orc = Oracle(h_root=r.h_root())
