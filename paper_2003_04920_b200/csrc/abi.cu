@@ -195,6 +195,7 @@ struct pirrt_ctx {
                                                              // above k * warps); 0: block-chunked edge-parallel
     int wq_keep = 32;                                        // PIRRT_WQ_KEEP
     int wq_tail = -1;                                        // PIRRT_WQ_TAIL (-1: 16 per block)
+    int wq_wide = -1;                                        // PIRRT_WQ_WIDE (-1: 10 per block, 0: off)
     int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
@@ -427,6 +428,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_HALVES")) c->halves = std::max(0, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_WQ_KEEP")) c->wq_keep = std::max(1, std::min(64, std::atoi(w)));
     if (const char* w = std::getenv("PIRRT_WQ_TAIL")) c->wq_tail = std::atoi(w);
+    if (const char* w = std::getenv("PIRRT_WQ_WIDE")) c->wq_wide = std::atoi(w);
     if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
@@ -630,6 +632,7 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.wq_keep = c->wq_keep;
     // the hand-over frontier must fit the blocks' local frontiers (64 each)
     a.wq_tail = c->wq_tail < 0 ? 16 * c->grid_blocks : std::min(c->wq_tail, 64 * c->grid_blocks);
+    a.wq_wide = c->wq_wide < 0 ? 10 * c->grid_blocks : c->wq_wide;
     a.halves = c->halves;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
     a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;

@@ -126,6 +126,7 @@ struct ExploitArgs {
     int wq_keep;                      // work-queue Evaluate: items a block keeps per local level
     int wq_tail;                      // level-synchronous: hand a shrinking frontier of at most
                                       // this many items to the work queue (0: never)
+    int wq_wide;                      // ... and any frontier of at least this many (0: never)
     int debug;                        // PIRRT_DEBUG: device diagnostics
 };
 

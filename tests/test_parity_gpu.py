@@ -276,15 +276,16 @@ def test_sharded_loop_6d(P):
     dual_replay(gpu, orc, r, 1000)
 
 
-@pytest.mark.parametrize("bfs,keep,halves,tail", [("level", None, "1", "0"), ("level", None, "4", None),
-                                                  ("level", "2", None, "100000"),
-                                                  ("level", None, None, "0"),
-                                                  ("wq", "1", None, None), ("wq", "7", None, None),
-                                                  ("wq", "64", None, None)])
-def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves, tail):
+@pytest.mark.parametrize("bfs,keep,halves,tail,wide", [
+    ("level", None, "1", "0", "0"), ("level", None, "4", None, "0"),
+    ("level", "2", None, "100000", "0"), ("level", None, None, "0", "0"),
+    ("level", None, None, None, "5"), ("level", "3", None, "0", "40"),
+    ("wq", "1", None, None, None), ("wq", "7", None, None, None), ("wq", "64", None, None, None)])
+def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves, tail, wide):
     # the Evaluate variants must agree with the oracle: level-synchronous
     # (block-chunked or one warp per item, 16-lane items from small frontiers
-    # on, with or without handing the shrinking tail to the work queue), and
+    # on, with or without handing the shrinking tail or a wide frontier to
+    # the work queue), and
     # the work queue from the root (its local frontier size wq_keep decides
     # how much goes through the global queue)
     monkeypatch.setenv("PIRRT_BFS", bfs)
@@ -294,6 +295,8 @@ def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves, tail):
         monkeypatch.setenv("PIRRT_HALVES", halves)
     if tail:
         monkeypatch.setenv("PIRRT_WQ_TAIL", tail)
+    if wide:
+        monkeypatch.setenv("PIRRT_WQ_WIDE", wide)
     r = gen.rrg(2, 4000, gen.gamma_star(2), n_boxes=25, seed=gen.seed_of("async"))
     gpu = P.Context(h_root=r.h_root())
     orc = Oracle(h_root=r.h_root())
@@ -306,6 +309,19 @@ def test_work_queue_small_grids_6d(P, monkeypatch, gb):
     monkeypatch.setenv("PIRRT_BFS", "wq")
     monkeypatch.setenv("PIRRT_WQ_KEEP", "3")
     r = gen.rrg(6, 8000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("wq-small", gb))
+    gpu = P.Context(h_root=r.h_root(), grid_blocks=gb)
+    orc = Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, 700)
+
+
+@pytest.mark.parametrize("gb", [1, 3])
+def test_level_to_work_queue_handover_6d(P, monkeypatch, gb):
+    # level-synchronous start, hand-over to the work queue at a wide or a
+    # shrinking frontier, with few blocks and small local frontiers
+    monkeypatch.setenv("PIRRT_WQ_WIDE", "20")
+    monkeypatch.setenv("PIRRT_WQ_TAIL", "50")
+    monkeypatch.setenv("PIRRT_WQ_KEEP", "4")
+    r = gen.rrg(6, 8000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("handover", gb))
     gpu = P.Context(h_root=r.h_root(), grid_blocks=gb)
     orc = Oracle(h_root=r.h_root())
     dual_replay(gpu, orc, r, 700)
