@@ -19,6 +19,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 PRUNE_OFF = 1
 VALIDATE = 2
 EDGES_UNDIRECTED = 4
+PARENT_FORM = 8
 
 
 class OracleError(RuntimeError):
@@ -75,7 +76,8 @@ def _load():
     lib.orc_evaluate_step.argtypes = [P, P, P, P]
     lib.orc_get_state.argtypes = [P, P, P, P, P, C.c_int64]
     lib.orc_set_policy.argtypes = [P, P, P, P]
-    lib.orc_best_path.argtypes = [P, P, C.c_int64, P, P]
+    lib.orc_best_path.argtypes = [P, P, C.c_int64, P, P, P]
+    lib.orc_set_goals.argtypes = [P, P, C.c_int32]
     _lib = lib
     return lib
 
@@ -158,9 +160,19 @@ class Oracle:
             b = np.ascontiguousarray(b, dtype=np.uint8)
         self._check(self._lib.orc_set_policy(self._c, _ptr(parent), _ptr(g), _ptr(b)))
 
-    def best_path(self):
+    def set_goals(self, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        self._check(self._lib.orc_set_goals(self._c, _ptr(ids), int(ids.size)))
+
+    def best_path_goal(self):
+        """(path root..goal, cost, best goal id or -1)."""
         cap = self.n
         path = np.empty(max(cap, 1), np.int32)
-        ln = np.zeros(1, np.int64); cost = np.zeros(1, np.float64)
-        self._check(self._lib.orc_best_path(self._c, _ptr(path), cap, _ptr(ln), _ptr(cost)))
-        return path[: int(ln[0])].copy(), float(cost[0])
+        ln = np.zeros(1, np.int64); cost = np.zeros(1, np.float64); goal = np.zeros(1, np.int32)
+        self._check(self._lib.orc_best_path(self._c, _ptr(path), cap, _ptr(ln), _ptr(cost),
+                                            _ptr(goal)))
+        return path[: int(ln[0])].copy(), float(cost[0]), int(goal[0])
+
+    def best_path(self):
+        path, cost, _ = self.best_path_goal()
+        return path, cost

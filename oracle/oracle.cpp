@@ -17,6 +17,7 @@
 // DESIGN.md section 3).
 #include "oracle.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -48,6 +49,9 @@ struct orc_ctx {
     int32_t max_iterations;
     uint32_t flags;
     int64_t n_edges;
+    // goal set G = {x_goal} u extra goal ids (reading R4, goal-set form),
+    // sorted ascending; ids >= |V| are inactive until appended
+    std::vector<int32_t> goals;
 };
 
 static const int32_t kRoot = 0;  // x_init
@@ -75,6 +79,7 @@ extern "C" orc_ctx* orc_create(double h_root, double h_goal, double epsilon,
     c->max_iterations = max_iterations;
     c->flags = flags;
     c->n_edges = 0;
+    c->goals = {1};
     return c;
 }
 
@@ -84,8 +89,39 @@ extern "C" int64_t orc_num_vertices(const orc_ctx* c) {
     return (int64_t)c->g.size();
 }
 
-// Goal cost used as the promising threshold: g(x_goal).
-static double goal_cost(const orc_ctx* c) { return c->g[kGoal]; }
+static bool is_goal(const orc_ctx* c, int64_t v) {
+    return std::binary_search(c->goals.begin(), c->goals.end(), (int32_t)v);
+}
+
+// Goal cost used as the promising threshold: g(x_goal); for
+// a goal set, the minimum over the goals that exist among the first n_exist
+// vertices (R4).  *best receives the best goal: the lowest id attaining the
+// minimum, or -1 if every such goal has g = +inf.
+static double goal_cost(const orc_ctx* c, int64_t n_exist, int32_t* best = nullptr) {
+    double m = kInf;
+    int32_t arg = -1;
+    for (int32_t t : c->goals) {          // ascending ids: strict < keeps the lowest
+        if (t >= n_exist) break;
+        if (c->g[t] < m) { m = c->g[t]; arg = t; }
+    }
+    if (best) *best = arg;
+    return m;
+}
+
+// Extra goal vertices (R4, goal-set form): G = {x_goal} u ids.  Ids may name
+// vertices not appended yet; they join G when they exist.
+extern "C" int orc_set_goals(orc_ctx* c, const int32_t* ids, int32_t n) {
+    if (n < 0 || (n > 0 && !ids)) return fail(-1, "set_goals: bad arguments");
+    std::vector<int32_t> gs = {1};
+    for (int32_t i = 0; i < n; ++i) {
+        if (ids[i] < 1) return fail(-2, "set_goals: goal id must be >= 1 (not the root)");
+        gs.push_back(ids[i]);
+    }
+    std::sort(gs.begin(), gs.end());
+    gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+    c->goals = gs;
+    return 0;
+}
 
 // Append one batch: S new vertices and their edges (Alg. 3 lines 6-8,
 // PAPER.md:456-460), then the "small exploitation" of Extend on each new
@@ -162,7 +198,10 @@ extern "C" int orc_append(orc_ctx* c, int32_t n_new, const double* h_new,
         }
     }
     // ---- commit: vertices (SoA) and edges (COO -> in-lists) ----
-    const double thr = goal_cost(c);  // g(x_goal) is an old vertex: fixed here
+    // promising threshold of the new vertices: the goal cost before the
+    // batch (old goals only; a new goal vertex does not lower it for its own
+    // batch), so the test does not depend on the order inside the batch
+    const double thr = goal_cost(c, n_old);
     c->g.resize(n_all, kInf);
     c->h.resize(n_all, 0.0);
     c->pc.resize(n_all, 0.0);
@@ -224,7 +263,7 @@ static void improve(orc_ctx* c, double* dg_out, int32_t* changed_out,
     int64_t relax = 0;
     for (int64_t v = 0; v < n; ++v) {
         if (v == kRoot) continue;
-        if (!(prune_off || c->b[v] || v == kGoal)) continue;
+        if (!(prune_off || c->b[v] || is_goal(c, v))) continue;
         double best = kInf;
         int32_t arg = -1;
         double argc = 0.0;
@@ -257,7 +296,8 @@ static void improve(orc_ctx* c, double* dg_out, int32_t* changed_out,
 static void evaluate(orc_ctx* c, int32_t* changed_out, int64_t* visits_out,
                      int32_t* levels_out) {
     const int64_t n = (int64_t)c->g.size();
-    const double thr = (c->flags & ORC_F_PRUNE_OFF) ? kInf : goal_cost(c);
+    const double thr = (c->flags & ORC_F_PRUNE_OFF) ? kInf : goal_cost(c, n);
+    const bool parent_form = (c->flags & ORC_F_PARENT_FORM) != 0;
     // child(T, v) = { n : parent(n) == v }, listed in id order.
     std::vector<std::vector<int32_t>> kids(n);
     for (int64_t v = 0; v < n; ++v)
@@ -277,7 +317,11 @@ static void evaluate(orc_ctx* c, int32_t* changed_out, int64_t* visits_out,
                 c->g[v] = c->g[p] + c->pc[v];  // g(n) <- c(v,n) + g(v)
                 ++visits;
                 visited = true;
-                if (c->g[v] + c->h[v] < thr) {  // P:263, child form (R2)
+                // child form (R2) g(n) + h(n) < thr, or the literal
+                // parent form h(v) + g(v) < thr (NEXT-4 variant)
+                const bool pass = parent_form ? (c->g[p] + c->h[p] < thr)
+                                              : (c->g[v] + c->h[v] < thr);
+                if (pass) {
                     c->b[v] = 1;                // B <- B u {n}
                     next.push_back(v);          // push(Q, n)
                 }
@@ -391,19 +435,22 @@ extern "C" int orc_set_policy(orc_ctx* c, const int32_t* parent,
     return 0;
 }
 
-// Policy-tree extraction (Alg. 1 lines 8-12): the goal
-// branch of the tree, root..goal.  Unreached goal: length 0, cost +inf.
+// Policy-tree extraction (Alg. 1 lines 8-12): the branch
+// of the best goal (lowest g, lowest id on ties), root..goal.  Unreached
+// goal set: length 0, cost +inf, goal -1.
 extern "C" int orc_best_path(const orc_ctx* c, int32_t* path, int64_t cap,
-                             int64_t* len, double* cost) {
+                             int64_t* len, double* cost, int32_t* goal) {
     const int64_t n = (int64_t)c->g.size();
-    double gc = c->g[kGoal];
+    int32_t best = -1;
+    double gc = goal_cost(c, n, &best);   // best goal: lowest id at the minimum (R4, R6)
     if (std::isinf(gc)) {
         if (len) *len = 0;
         if (cost) *cost = kInf;
+        if (goal) *goal = -1;
         return 0;
     }
     std::vector<int32_t> rev;
-    int32_t v = kGoal;
+    int32_t v = best;
     while (v != -1) {
         rev.push_back(v);
         if ((int64_t)rev.size() > n) return fail(-8, "best_path: parent cycle");
@@ -414,5 +461,6 @@ extern "C" int orc_best_path(const orc_ctx* c, int32_t* path, int64_t cap,
     for (size_t i = 0; i < rev.size(); ++i) path[i] = rev[rev.size() - 1 - i];
     if (len) *len = (int64_t)rev.size();
     if (cost) *cost = gc;
+    if (goal) *goal = best;
     return 0;
 }

@@ -30,6 +30,8 @@ typedef struct orc_ctx orc_ctx;
 #define ORC_F_PRUNE_OFF 1u        /* I = V \ {root}, thr = +inf (classical PI) */
 #define ORC_F_VALIDATE 2u         /* duplicate-edge and g_new consistency checks */
 #define ORC_F_EDGES_UNDIRECTED 4u /* append: each (src,dst,cost) stored both ways */
+#define ORC_F_PARENT_FORM 8u      /* Evaluate tests the parent, h(v)+g(v) < thr, as
+                                     printed at PAPER.md:263 (NEXT-4 variant of R2) */
 
 typedef struct {
     int32_t iterations;     /* number of Improve calls (Alg. 2)            */
@@ -55,6 +57,11 @@ int orc_append(orc_ctx* c, int32_t n_new, const double* h_new,
 
 int orc_exploit(orc_ctx* c, orc_stats* out);
 
+/* Goal set (reading R4, goal-set form): G = {x_goal} u ids[0..n).  Ids may
+ * name vertices appended later.  Threshold = min over existing goals of g;
+ * every existing goal is in the Improve set. */
+int orc_set_goals(orc_ctx* c, const int32_t* ids, int32_t n);
+
 /* single steps, for the worked-example pins */
 int orc_improve_step(orc_ctx* c, double* delta_g, int32_t* parent_changed,
                      int64_t* relaxations);
@@ -66,7 +73,7 @@ int orc_get_state(const orc_ctx* c, int32_t* parent, double* g, double* pc,
 int orc_set_policy(orc_ctx* c, const int32_t* parent, const double* g,
                    const uint8_t* b);
 int orc_best_path(const orc_ctx* c, int32_t* path, int64_t cap, int64_t* len,
-                  double* cost);
+                  double* cost, int32_t* goal);
 
 #ifdef __cplusplus
 }

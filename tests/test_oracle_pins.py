@@ -200,13 +200,26 @@ def test_local_relaxation_on_id_dag_equals_dijkstra():
 
 # --------------------------------------------- P2: promising-subgraph certificate
 
-def certificate(o, src, dst, cost):
-    """Bellman certificate on S = B u {goal} (north_star: 'PI's fixed point
+def certificate(o, src, dst, cost, goals=(1,)):
+    """Bellman certificate on S = B u G (north_star: 'PI's fixed point
     must equal the shortest-path tree on the promising subgraph')."""
     parent, g, pc, b = o.state()
     n = g.size
-    S = set(np.nonzero(b)[0].tolist()) | {1}
     lists = in_lists(n, src, dst, cost)
+    S = set(np.nonzero(b)[0].tolist())
+    for t in goals:
+        t = int(t)
+        if t >= n or b[t]:
+            continue
+        best = min(((g[u] + c, u) for u, c in lists[t]), default=(INF, -1))
+        if best[0] < g[t]:
+            # a goal outside B whose best parent is not expanded keeps a stale
+            # g: Improve re-selects the SAME parent and the R13 stall guard
+            # ends the loop (a single goal cannot be in this state: its best
+            # parent beats thr = g(goal) and is expanded)
+            assert best[1] == parent[t]
+        else:
+            S.add(t)
     for v in S:                                     # no strict improvement (R5)
         for u, c in lists[v]:
             assert not (g[u] + c < g[v])
