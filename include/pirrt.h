@@ -57,6 +57,8 @@ enum {
     PIRRT_F_PRUNE_OFF = 1u,        /* I = V \ {root}, thr = +inf: classical PI (test/cold mode) */
     PIRRT_F_VALIDATE = 2u,         /* extra checks: g_new consistency                           */
     PIRRT_F_SHARDED = 16u,         /* use the sharded (NCCL) exploit loop even with nranks == 1 */
+    PIRRT_F_PARENT_FORM = 32u,     /* Evaluate's promising test on the parent v, h(v)+g(v) < thr,
+                                      as printed at PAPER.md:263 (variant of reading R2)         */
     /* append flags */
     PIRRT_F_EDGES_UNDIRECTED = 4u, /* each (src,dst,cost) is stored in both directions         */
     PIRRT_F_DEVICE_PTRS = 8u       /* input arrays are device pointers (e.g. torch CUDA tensors)*/
@@ -70,7 +72,7 @@ typedef struct {
     double h_goal;            /* h(x_goal); default 0                                       */
     double epsilon;           /* stop when Delta g <= epsilon (R5); default 0               */
     int32_t max_iterations;   /* Improve cap per exploit; 0 -> 10 |V| (R11)                  */
-    uint32_t flags;           /* PIRRT_F_PRUNE_OFF | PIRRT_F_VALIDATE                        */
+    uint32_t flags;           /* PIRRT_F_PRUNE_OFF | PIRRT_F_VALIDATE | PIRRT_F_PARENT_FORM  */
     int32_t device;           /* CUDA device ordinal                                        */
     void* stream;             /* cudaStream_t to run on (e.g. a torch stream); NULL: own one */
     int32_t grid_blocks;      /* persistent-kernel grid; 0 = auto (SMs x occupancy)          */
@@ -78,6 +80,16 @@ typedef struct {
     int32_t rank;             /* this process's rank                                        */
     const void* nccl_unique_id; /* ncclUniqueId (128 B, pirrt_nccl_unique_id on one rank,
                                    broadcast by the caller) when nranks > 1; NULL otherwise  */
+    /* Goal set (reading R4, goal-set form; the paper's case is the single
+     * x_goal): G = {x_goal} u goals[0..n_goals).  Ids must be >= 1 and may name
+     * vertices appended later (a goal joins G when its vertex exists).  The
+     * promising threshold is min over existing goals of g (P:263 with R3);
+     * every existing goal is in the Improve set; best_path follows the best
+     * goal (lowest g, lowest id on ties).  New vertices of a batch are
+     * promising against the goal cost before that batch.  Copied at create;
+     * NULL/0 = {x_goal}.  E_RANGE: an id < 1. */
+    const pirrt_vid* goals;
+    int32_t n_goals;
 } pirrt_config;
 
 typedef struct {
@@ -150,12 +162,14 @@ int pirrt_get_costs(const pirrt_ctx* ctx, double* g_out, int64_t cap);
 int pirrt_get_promising(const pirrt_ctx* ctx, uint8_t* b_out, int64_t cap);
 int pirrt_get_parent_costs(const pirrt_ctx* ctx, double* pc_out, int64_t cap);
 
-/* Policy-tree extraction (Alg. 1 lines 8-12): the goal
- * branch root..x_goal into path_out[0..len).  Unreached goal: *len_out = 0,
- * *cost_out = +inf.  E_RANGE if cap < path length (nothing written);
+/* Policy-tree extraction (Alg. 1 lines 8-12): the branch
+ * root..goal of the best goal (lowest g over the goal set, lowest id on ties;
+ * reading R4) into path_out[0..len); *cost_out = its g, *goal_out = its id
+ * (outputs nullable).  No goal reached: *len_out = 0, *cost_out = +inf,
+ * *goal_out = -1.  E_RANGE if cap < path length (nothing written);
  * E_CORRUPT if the branch does not reach the root. */
 int pirrt_best_path(const pirrt_ctx* ctx, pirrt_vid* path_out, int64_t cap,
-                    int64_t* len_out, double* cost_out);
+                    int64_t* len_out, double* cost_out, pirrt_vid* goal_out);
 
 /* Restore a policy snapshot (host arrays of length n): parent, g, and b
  * (nullable -> B = {}).  The policy-edge cost of v is re-read from the stored

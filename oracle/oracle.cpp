@@ -59,6 +59,26 @@ static const int32_t kGoal = 1;  // x_goal
 
 extern "C" const char* orc_last_error(void) { return g_err.c_str(); }
 
+// Does the parent array p[0..n) contain a cycle (the
+// policy is a tree)?  Plain three-colour walk up the parent chains.
+static bool has_parent_cycle(const std::vector<int32_t>& p) {
+    const size_t n = p.size();
+    std::vector<uint8_t> state(n, 0);   // 0 unseen, 1 on the current walk, 2 done
+    std::vector<int32_t> walk;
+    for (size_t s = 0; s < n; ++s) {
+        walk.clear();
+        int32_t v = (int32_t)s;
+        while (v >= 0 && (size_t)v < n && state[v] == 0) {
+            state[v] = 1;
+            walk.push_back(v);
+            v = p[v];
+        }
+        if (v >= 0 && (size_t)v < n && state[v] == 1) return true;   // came back onto this walk
+        for (int32_t w : walk) state[w] = 2;
+    }
+    return false;
+}
+
 extern "C" orc_ctx* orc_create(double h_root, double h_goal, double epsilon,
                                int32_t max_iterations, uint32_t flags) {
     // Alg. 1 line 1: V <- {x_init, x_goal}, E <- {}, B <- {}.
@@ -196,6 +216,11 @@ extern "C" int orc_append(orc_ctx* c, int32_t n_new, const double* h_new,
                 for (size_t j = i + 1; j < s.size(); ++j)
                     if (s[i] == s[j]) return fail(-1, "append: duplicate edge");
         }
+    }
+    if (parent_new && ((flags | c->flags) & ORC_F_VALIDATE)) {
+        std::vector<int32_t> p(c->parent);
+        p.insert(p.end(), parent_new, parent_new + n_new);
+        if (has_parent_cycle(p)) return fail(-8, "append: given policy has a parent cycle");
     }
     // ---- commit: vertices (SoA) and edges (COO -> in-lists) ----
     // promising threshold of the new vertices: the goal cost before the
@@ -425,6 +450,10 @@ extern "C" int orc_set_policy(orc_ctx* c, const int32_t* parent,
                 if (uc.first == p) { pc[v] = uc.second; found = true; break; }
             if (!found) return fail(-1, "set_policy: parent edge not in graph");
         }
+    }
+    if (c->flags & ORC_F_VALIDATE) {
+        if (has_parent_cycle(std::vector<int32_t>(parent, parent + n)))
+            return fail(-8, "set_policy: parent cycle");
     }
     for (int64_t v = 0; v < n; ++v) {
         c->parent[v] = parent[v];

@@ -66,6 +66,8 @@ std::string err_bits(int e) {
     if (e & kErrGNew) m += " bad g (given policy);";
     if (e & kErrPcMissing) m += " policy edge (parent -> v) not stored;";
     if (e & kErrRoot) m += " root must have parent -1 and g 0;";
+    if (e & kErrDup) m += " duplicate (src,dst) edge (VALIDATE);";
+    if (e & kErrCycle) m += " parent cycle (VALIDATE);";
     return m;
 }
 
@@ -199,6 +201,9 @@ struct pirrt_ctx {
     int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
+    // goal set G (R4): sorted unique ids incl. x_goal (device copy + host copy)
+    int* goals = nullptr; int64_t goals_cap = 0;
+    std::vector<int> goals_host;
 };
 
 namespace {
@@ -315,7 +320,7 @@ void free_all(pirrt_ctx* c) {
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
                     c->qv, c->qg, c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
-                    c->rec_local, c->rec_all, c->rec_counts, c->app_bsum};
+                    c->rec_local, c->rec_all, c->rec_counts, c->app_bsum, c->goals};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
@@ -415,12 +420,24 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         return fail(PIRRT_E_INVAL, "create: bad nranks/rank");
     if (cfg.nranks > 1 && !cfg.nccl_unique_id)
         return fail(PIRRT_E_INVAL, "create: nranks > 1 needs nccl_unique_id");
+    if (cfg.n_goals < 0 || (cfg.n_goals > 0 && !cfg.goals))
+        return fail(PIRRT_E_INVAL, "create: bad goals/n_goals");
+    std::vector<int> goal_ids = {kGoal};
+    for (int32_t i = 0; i < cfg.n_goals; ++i) {
+        if (cfg.goals[i] < 1 || cfg.goals[i] >= kMaxVertices)
+            return fail(PIRRT_E_RANGE, "create: goal id must be >= 1 (not the root)");
+        goal_ids.push_back(cfg.goals[i]);
+    }
+    std::sort(goal_ids.begin(), goal_ids.end());
+    goal_ids.erase(std::unique(goal_ids.begin(), goal_ids.end()), goal_ids.end());
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (cfg.device < 0 || cfg.device >= ndev) return fail(PIRRT_E_INVAL, "create: bad device");
     CU(cudaSetDevice(cfg.device));
     pirrt_ctx* c = new pirrt_ctx();
     c->cfg = cfg;
+    c->cfg.goals = nullptr;                     // the caller's array is not kept
+    c->goals_host = goal_ids;
     if (const char* w = std::getenv("PIRRT_WATCHDOG_MS"))
         c->watchdog_ns = (unsigned long long)std::strtoull(w, nullptr, 10) * 1000000ull;
     if (const char* w = std::getenv("PIRRT_COMPACT_MIN")) c->compact_min = std::atof(w);
@@ -474,6 +491,10 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if ((rc = grow(c->app_bsum, c->app_bsum_cap, 2 * kAppendMaxBlocks + 2, 0, c->stream))) return bail(rc);
     for (int k = 0; k < 2; ++k)
         if ((rc = grow(c->odidx[k], c->odidx_cap[k], ecap0, 0, c->stream))) return bail(rc);
+    if ((rc = grow(c->goals, c->goals_cap, (int64_t)goal_ids.size(), 0, c->stream))) return bail(rc);
+    if (cudaMemcpyAsync(c->goals, goal_ids.data(), goal_ids.size() * sizeof(int),
+                        cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        return bail(fail(PIRRT_E_CUDA, "create: goals copy"));
     if (cudaMalloc(&c->ctl, sizeof(DevCtl)) != cudaSuccess) return bail(fail(PIRRT_E_NOMEM, "ctl"));
     if (cudaMallocHost(&c->ctl_host, sizeof(DevCtl)) != cudaSuccess)
         return bail(fail(PIRRT_E_NOMEM, "ctl host"));
@@ -589,16 +610,24 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     a.n_old = n_old; a.n_new = n_new; a.base_edges = c->base_edges;
     a.ctl = c->ctl;
     a.grid_blocks = c->num_sms;
+    a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
     const long long l0 = g_kernel_launches;
     cudaError_t e = c->fused_append
         ? launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks, c->l2win, s)
         : launch_append(a, s);
+    if (e == cudaSuccess && a.validate) {
+        // VALIDATE: duplicates against the stored graph and inside the batch;
+        // a given policy must not close a parent cycle
+        e = launch_dup_check(a, s);
+        if (e == cudaSuccess && parent_new) e = launch_cycle_check(c->parent, n_all, (int*)c->cnt, c->ctl, s);
+    }
     c->launches += g_kernel_launches - l0;
     if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("append: ") + cudaGetErrorString(e)); }
     if ((rc = read_ctl(c))) { c->broken = true; return rc; }
     const int err = c->ctl_host->err;
     if (err) {
-        int code = (err & (kErrRange)) ? PIRRT_E_RANGE : PIRRT_E_INVAL;
+        int code = (err & (kErrRange)) ? PIRRT_E_RANGE
+                 : (err & kErrCycle && !(err & ~kErrCycle)) ? PIRRT_E_CORRUPT : PIRRT_E_INVAL;
         return fail(code, "append rejected:" + err_bits(err));
     }
     // commit
@@ -636,6 +665,8 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.halves = c->halves;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
     a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;
+    a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
+    a.parent_form = (c->cfg.flags & PIRRT_F_PARENT_FORM) ? 1 : 0;
 }
 
 // Sharded exploit: per PI iteration
@@ -792,7 +823,7 @@ int pirrt_get_parent_costs(const pirrt_ctx* c, double* out, int64_t cap) {
 }
 
 int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64_t* len_out,
-                    double* cost_out) {
+                    double* cost_out, pirrt_vid* goal_out) {
     pirrt_ctx* c = const_cast<pirrt_ctx*>(cc);
     if (!c) return fail(PIRRT_E_INVAL, "best_path: NULL context");
     int rc;
@@ -802,7 +833,7 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     // only for paths longer than that
     constexpr int kHead = 1020;
     const long long l0 = g_kernel_launches;
-    CU(launch_best_path(c->parent, c->g, c->n, c->path, s));
+    CU(launch_best_path(c->parent, c->g, c->n, c->goals, (int)c->goals_host.size(), c->path, s));
     c->launches += g_kernel_launches - l0;
     const int first = std::min<int64_t>(kHead, c->n + 1);
     std::vector<int> buf(4 + first);
@@ -814,6 +845,7 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     if (std::isinf(gg)) {
         if (len_out) *len_out = 0;
         if (cost_out) *cost_out = INFINITY;
+        if (goal_out) *goal_out = -1;
         return PIRRT_OK;
     }
     if (len < 0) return fail(PIRRT_E_CORRUPT, "best_path: parent cycle");
@@ -831,6 +863,7 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     for (int i = 0; i < len; ++i) path_out[i] = rev[len - 1 - i];
     if (len_out) *len_out = len;
     if (cost_out) *cost_out = gg;
+    if (goal_out) *goal_out = buf[1];
     return PIRRT_OK;
 }
 
@@ -866,11 +899,14 @@ int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, con
     a.n = n; a.ctl = c->ctl;
     const long long l0 = g_kernel_launches;
     CU(launch_set_policy(a, s));
+    if (c->cfg.flags & PIRRT_F_VALIDATE) CU(launch_cycle_check(d_parent, n, (int*)c->cnt, c->ctl, s));
     c->launches += g_kernel_launches - l0;
     if ((rc = read_ctl(c))) return rc;
     if (c->ctl_host->err) {
         const int err = c->ctl_host->err;
-        return fail((err & kErrRange) ? PIRRT_E_RANGE : PIRRT_E_INVAL, "set_policy rejected:" + err_bits(err));
+        const int code = (err & kErrRange) ? PIRRT_E_RANGE
+                       : (err & kErrCycle) ? PIRRT_E_CORRUPT : PIRRT_E_INVAL;
+        return fail(code, "set_policy rejected:" + err_bits(err));
     }
     // commit (g canonicalised: -0.0 -> +0.0 is irrelevant for validated g >= 0)
     CU(cudaMemcpyAsync(c->parent, d_parent, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, s));

@@ -22,7 +22,8 @@ constexpr unsigned kFull = 0xffffffffu;
 // validation error bits (append / set_policy)
 enum : int {
     kErrRange = 1, kErrSelfLoop = 2, kErrCost = 4, kErrH = 8,
-    kErrParent = 16, kErrPcMissing = 32, kErrGNew = 64, kErrRoot = 128
+    kErrParent = 16, kErrPcMissing = 32, kErrGNew = 64, kErrRoot = 128,
+    kErrDup = 256, kErrCycle = 512    // VALIDATE: duplicate (src,dst); parent cycle
 };
 
 // Per-iteration counters of the exploit loop, double-buffered by iteration
@@ -128,7 +129,39 @@ struct ExploitArgs {
                                       // this many items to the work queue (0: never)
     int wq_wide;                      // ... and any frontier of at least this many (0: never)
     int debug;                        // PIRRT_DEBUG: device diagnostics
+    // goal set G (R4): sorted ascending ids, contains x_goal; ids >= n inactive
+    const int* goals;
+    int n_goals;
+    int parent_form;                  // PIRRT_F_PARENT_FORM: P:263 literal test (NEXT-4)
 };
+
+// ---- goal set (reading R4, goal-set form) ----
+// v in G?  G is sorted; the single-goal case is the paper's x_goal.
+__device__ __forceinline__ bool is_goal(const int* goals, int n_goals, int v) {
+    if (n_goals == 1) return v == kGoal;
+    int lo = 0, hi = n_goals - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(&goals[mid]) < v) lo = mid + 1; else hi = mid;
+    }
+    return __ldg(&goals[lo]) == v;
+}
+
+// Goal cost min over the goals among the first n_exist vertices of g (the
+// promising threshold, P:263 with R3/R4).  Warp-collective: every lane of a
+// converged warp calls it and receives the value.
+__device__ __forceinline__ double warp_goal_cost(const double* g, const int* goals, int n_goals,
+                                                 int n_exist) {
+    if (n_goals == 1) return *(volatile const double*)&g[kGoal];
+    double m = INFINITY;
+    for (int i = (threadIdx.x & 31); i < n_goals; i += 32) {
+        const int t = __ldg(&goals[i]);
+        if (t < n_exist) m = fmin(m, *(volatile const double*)&g[t]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmin(m, __shfl_xor_sync(kFull, m, o));
+    return m;
+}
 
 // kernels launched by this host thread (diagnostics; abi.cu attributes the
 // delta of each call to its context)
@@ -183,6 +216,8 @@ struct AppendArgs {
     int Bcount;
     DevCtl* ctl;
     int grid_blocks;
+    const int* goals;             // goal set (R4); the promising threshold of the
+    int n_goals;                  // new vertices is the goal cost before the batch
 };
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t s);
 // one cooperative kernel for the whole append; bsum needs 2 * max_blocks entries
@@ -209,12 +244,20 @@ struct PolicyArgs {
 };
 cudaError_t launch_set_policy(const PolicyArgs& a, cudaStream_t s);
 
+// VALIDATE: a staged batch whose edges duplicate a
+// stored (src,dst) pair or each other -> kErrDup (run after the append merged
+// the batch into the new delta, before the host commits); a parent array with
+// a cycle -> kErrCycle (integer pointer jumping; tmp holds 2 n ints).
+cudaError_t launch_dup_check(const AppendArgs& a, cudaStream_t s);
+cudaError_t launch_cycle_check(const int* parent, int n, int* tmp, DevCtl* ctl, cudaStream_t s);
+
 // B list = {v : b[v] == 1} in ascending order into list[1..]; count -> *count_out
 cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* count_out,
                                  long long* cnt, long long* scan_tmp, cudaStream_t s);
 
-cudaError_t launch_best_path(const int* parent, const double* g, int n, int* out,
-                             cudaStream_t s);
+// best goal (lowest g, lowest id on ties) and its branch; see k_best_path
+cudaError_t launch_best_path(const int* parent, const double* g, int n, const int* goals,
+                             int n_goals, int* out, cudaStream_t s);
 
 // device-wide exclusive scan: out[0..L] with out[L] = total
 cudaError_t scan_exclusive(const long long* in, long long* out, long long L,

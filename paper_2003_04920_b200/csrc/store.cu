@@ -348,11 +348,13 @@ __global__ void __launch_bounds__(kBT) k_relax_new(
 
 // b(v) = g(v) + h(v) < g(x_goal) for the new vertices;
 // promising ones are appended to the B list (invisible until the host
-// commits the new count)
+// commits the new count).  Goal set (R4): the threshold is the goal cost
+// before the batch (goals among the old vertices).
 __global__ void k_new_promising(const double* g, const double* h, unsigned char* b, int n_old,
-                                int n_new, int* Blist, int Bcount, DevCtl* ctl) {
+                                int n_new, int* Blist, int Bcount, DevCtl* ctl, const int* goals,
+                                int n_goals) {
     if (failed(ctl)) return;
-    const double thr = g[kGoal];
+    const double thr = warp_goal_cost(g, goals, n_goals, n_old);
     const int lane = threadIdx.x & 31;
     for (int base = blockIdx.x * blockDim.x; base < n_new; base += gridDim.x * blockDim.x) {
         const int i = base + threadIdx.x;
@@ -430,15 +432,67 @@ __global__ void k_check_policy(const int* parent_in, const double* g_in, int n, 
     if (err) atomicOr(&ctl->err, err);
 }
 
-// out[0] = length (-1: cycle), out[1..2] = g(goal) bits, out[4..] = goal..root
-__global__ void k_best_path(const int* parent, const double* g, int n, int* out) {
-    int v = kGoal, len = 0;
+// VALIDATE duplicate check: staged edge e = (u -> v) (and v -> u when
+// undirected) is a duplicate iff u occurs more than once in v's in-row after
+// the merge (base row + the NEW delta row, which holds e itself).
+__global__ void k_dup_check(const int* src, const int* dst, long long m, int undirected,
+                            const long long* boff, const int* bidx, const long long* doff,
+                            const int* didx, int n_old, DevCtl* ctl) {
+    const int lane = threadIdx.x & 31;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long items = undirected ? 2 * m : m;
+    for (long long it = w0; it < items; it += nw) {        // one warp per directed edge
+        const long long e = undirected ? it >> 1 : it;
+        const bool rev = undirected && (it & 1);
+        const int u = rev ? dst[e] : src[e], v = rev ? src[e] : dst[e];
+        int cnt = 0;
+        if (v < n_old)
+            for (long long k = boff[v] + lane; k < boff[v + 1]; k += 32) cnt += bidx[k] == u;
+        for (long long k = doff[v] + lane; k < doff[v + 1]; k += 32) cnt += didx[k] == u;
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+        if (lane == 0 && cnt > 1) atomicOr(&ctl->err, kErrDup);
+    }
+}
+
+// Parent-cycle check by pointer jumping over the (integer) parent array:
+// after R rounds anc(v) is the 2^R-th ancestor, or -1 once the chain ended;
+// with 2^R >= n every acyclic chain has ended, so a remaining ancestor means
+// a cycle.  Integer work only (no re-associated sums of g).
+__global__ void k_jump(const int* in, int* out, int n, int first, const int* parent) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int x = first ? parent[v] : in[v];
+        out[v] = (x < 0 || x >= n) ? -1 : (first ? parent[x] : in[x]);
+    }
+}
+__global__ void k_jump_any(const int* anc, int n, DevCtl* ctl) {
+    int bad = 0;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        bad |= anc[v] >= 0;
+    if (bad) atomicOr(&ctl->err, kErrCycle);
+}
+
+// Best goal (R4: lowest g over the existing goals, lowest id on ties) and
+// its branch (Alg. 1 lines 8-12).
+// out[0] = length (-1: cycle), out[1] = best goal (-1: none reached),
+// out[2..3] = its g bits, out[4..] = goal..root
+__global__ void k_best_path(const int* parent, const double* g, int n, const int* goals,
+                            int n_goals, int* out) {
+    int best = -1;
+    double gb = INFINITY;
+    for (int i = 0; i < n_goals; ++i) {                 // ascending ids: strict < keeps the lowest
+        const int t = goals[i];
+        if (t >= n) break;
+        if (g[t] < gb) { gb = g[t]; best = t; }
+    }
+    out[1] = best;
+    *(double*)&out[2] = gb;
+    int v = best, len = 0;
     while (v != -1 && len <= n) {
         out[4 + len++] = v;
         v = parent[v];
     }
     out[0] = (v == -1) ? len : -1;
-    *(double*)&out[2] = g[kGoal];
 }
 
 
@@ -492,6 +546,13 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     const int lane = threadIdx.x & 31;
     const int gw = tid >> 5, nw = nthreads >> 5;
     long long* cnt0 = a.cnt;
+    // promising threshold of the new vertices: the goal cost before the batch
+    // (R4; g of old vertices is not written by an append), read once here
+    __shared__ double s_thr;
+    if (threadIdx.x < 32) {
+        const double t = warp_goal_cost(a.g, a.goals, a.n_goals, n_old);
+        if (threadIdx.x == 0) s_thr = t;
+    }
     // ---- P0 validation (R12)
     {
         int err = 0;
@@ -703,7 +764,8 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     grid.sync();
     if (failed(ctl)) return;
     // ---- P7 b(v) = g(v) + h(v) < g(x_goal); promising ones join the B list
-    const double thr = a.g[kGoal];
+    // (goal set, R4: the goal cost before the batch)
+    const double thr = s_thr;
     for (int base = blockIdx.x * blockDim.x; base < n_new; base += nthreads) {
         const int i = base + threadIdx.x;
         const int v = n_old + i;
@@ -744,6 +806,33 @@ cudaError_t scan_exclusive(const long long* in, long long* out, long long L, lon
     k_scan_apply<<<(unsigned)P, kBT, 0, s>>>(in, L, tmp, out);
     // out[L] = total = tmp[P]
     cudaMemcpyAsync(out + L, tmp + P, sizeof(long long), cudaMemcpyDeviceToDevice, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dup_check(const AppendArgs& a, cudaStream_t s) {
+    if (a.m == 0) return cudaSuccess;
+    const long long items = a.undirected ? 2 * a.m : a.m;
+    ++g_kernel_launches;
+    k_dup_check<<<grid_for(items * 32), kBT, 0, s>>>(a.src, a.dst, a.m, a.undirected, a.boff,
+                                                     a.bidx, a.doff_new, a.didx_new, a.n_old,
+                                                     a.ctl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cycle_check(const int* parent, int n, int* tmp, DevCtl* ctl, cudaStream_t s) {
+    if (n <= 1) return cudaSuccess;
+    int* buf[2] = {tmp, tmp + n};
+    // round 0 writes the 2nd ancestor; round r the 2^(r+1)-th
+    int r = 0, cur = 0;
+    ++g_kernel_launches;
+    k_jump<<<grid_for(n), kBT, 0, s>>>(nullptr, buf[0], n, 1, parent);
+    for (r = 1; (1LL << r) < (long long)n; ++r) {
+        ++g_kernel_launches;
+        k_jump<<<grid_for(n), kBT, 0, s>>>(buf[cur], buf[cur ^ 1], n, 0, nullptr);
+        cur ^= 1;
+    }
+    ++g_kernel_launches;
+    k_jump_any<<<grid_for(n), kBT, 0, s>>>(buf[cur], n, ctl);
     return cudaGetLastError();
 }
 
@@ -825,7 +914,7 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
         }
         ++g_kernel_launches;
         k_new_promising<<<grid_for(a.n_new), kBT, 0, s>>>(a.g, a.h, a.b, a.n_old, a.n_new, a.Blist,
-                                                          a.Bcount, a.ctl);
+                                                          a.Bcount, a.ctl, a.goals, a.n_goals);
     }
     return cudaGetLastError();
 }
@@ -876,10 +965,10 @@ cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* 
     return cudaGetLastError();
 }
 
-cudaError_t launch_best_path(const int* parent, const double* g, int n, int* out,
-                             cudaStream_t s) {
+cudaError_t launch_best_path(const int* parent, const double* g, int n, const int* goals,
+                             int n_goals, int* out, cudaStream_t s) {
     ++g_kernel_launches;
-    k_best_path<<<1, 1, 0, s>>>(parent, g, n, out);
+    k_best_path<<<1, 1, 0, s>>>(parent, g, n, goals, n_goals, out);
     return cudaGetLastError();
 }
 

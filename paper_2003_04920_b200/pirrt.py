@@ -36,6 +36,7 @@ PIRRT_F_VALIDATE = 2
 PIRRT_F_EDGES_UNDIRECTED = 4
 PIRRT_F_DEVICE_PTRS = 8
 PIRRT_F_SHARDED = 16
+PIRRT_F_PARENT_FORM = 32
 NCCL_UNIQUE_ID_BYTES = 128
 
 # every symbol include/pirrt.h declares (checked by tests/test_abi.py)
@@ -64,6 +65,8 @@ class pirrt_config(C.Structure):
         ("nranks", C.c_int32),
         ("rank", C.c_int32),
         ("nccl_unique_id", C.c_void_p),
+        ("goals", C.c_void_p),
+        ("n_goals", C.c_int32),
     ]
 
 
@@ -103,7 +106,7 @@ def _load():
     for f in ("pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
               "pirrt_get_parent_costs"):
         getattr(lib, f).argtypes = [P, P, C.c_int64]
-    lib.pirrt_best_path.argtypes = [P, P, C.c_int64, P, P]
+    lib.pirrt_best_path.argtypes = [P, P, C.c_int64, P, P, P]
     lib.pirrt_set_policy.argtypes = [P, P, P, P]
     lib.pirrt_num_vertices.argtypes = [P]
     lib.pirrt_num_vertices.restype = C.c_int64
@@ -211,7 +214,7 @@ class Context:
 
     def __init__(self, h_root=0.0, h_goal=0.0, epsilon=0.0, max_iterations=0, flags=0, device=0,
                  stream=None, vertex_capacity=0, edge_capacity=0, grid_blocks=0, nranks=1,
-                 rank=0, nccl_id: bytes | None = None):
+                 rank=0, nccl_id: bytes | None = None, goals=None):
         cfg = pirrt_config()
         pirrt_config_init(C.byref(cfg))
         cfg.h_root, cfg.h_goal, cfg.epsilon = float(h_root), float(h_goal), float(epsilon)
@@ -225,6 +228,10 @@ class Context:
             cfg.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p)
         if stream is not None:
             cfg.stream = int(getattr(stream, "cuda_stream", stream))
+        goal_arr = None
+        if goals is not None and len(goals) > 0:
+            goal_arr = np.ascontiguousarray(goals, dtype=np.int32)
+            cfg.goals, cfg.n_goals = goal_arr.ctypes.data, int(goal_arr.size)
         h = C.c_void_p()
         _check(pirrt_create(C.byref(cfg), C.byref(h)))
         self._h = h
@@ -305,13 +312,20 @@ class Context:
         """(parent, g, pc, b) -- same order as the oracle's state()."""
         return self.policy(), self.costs(), self.parent_costs(), self.promising()
 
-    def best_path(self):
+    def best_path_goal(self):
+        """(path root..goal, cost, best goal id or -1)."""
         cap = max(self.n, 1)
         path = np.empty(cap, np.int32)
         ln = C.c_int64(0)
         cost = C.c_double(0)
-        _check(pirrt_best_path(self._h, path.ctypes.data, cap, C.byref(ln), C.byref(cost)))
-        return path[: ln.value].copy(), float(cost.value)
+        goal = C.c_int32(0)
+        _check(pirrt_best_path(self._h, path.ctypes.data, cap, C.byref(ln), C.byref(cost),
+                               C.byref(goal)))
+        return path[: ln.value].copy(), float(cost.value), int(goal.value)
+
+    def best_path(self):
+        path, cost, _ = self.best_path_goal()
+        return path, cost
 
     def set_policy(self, parent, g, b=None):
         parent = np.ascontiguousarray(parent, np.int32)

@@ -59,7 +59,7 @@ def dual_replay(gpu, orc, graph, S, n_stop=None, undirected=True, check_every=1,
         gs, os_ = gpu.exploit(), orc.exploit()
         assert_same_stats(gs, os_, "final")
     assert_same_state(gpu, orc, "final")
-    gpath, gcost = gpu.best_path()
-    opath, ocost = orc.best_path()
-    assert np.array_equal(gpath, opath) and gcost == ocost
+    gpath, gcost, ggoal = gpu.best_path_goal()
+    opath, ocost, ogoal = orc.best_path_goal()
+    assert np.array_equal(gpath, opath) and gcost == ocost and ggoal == ogoal
     return k_ex

@@ -39,14 +39,30 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
+    # compile the C header with gcc and compare every field offset and the
+    # struct sizes with the ctypes mirrors of the binding
+    import subprocess
     from paper_2003_04920_b200 import pirrt
-    # sizes computed from the C declarations (x86-64 / aarch64 LP64 ABI)
-    assert C.sizeof(pirrt.pirrt_config) == 8 + 8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 8 + 4 + 4 + 4 + 4 + 8
-    assert C.sizeof(pirrt.pirrt_exploit_stats) == 4 + 4 + 8 + 8 + 8 + 4 * 4 + 4 * 4 + 8 + 8
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "pirrt.h"', 'int main(void) {']
+    for st in (pirrt.pirrt_config, pirrt.pirrt_exploit_stats):
+        lines.append(f'printf("{st.__name__} size %zu\\n", sizeof({st.__name__}));')
+        for f, _ in st._fields_:
+            lines.append(f'printf("{st.__name__} {f} %zu\\n", offsetof({st.__name__}, {f}));')
+    lines += ['return 0;', '}']
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for st in (pirrt.pirrt_config, pirrt.pirrt_exploit_stats):
+        assert got[(st.__name__, "size")] == C.sizeof(st)
+        for f, _ in st._fields_:
+            assert got[(st.__name__, f)] == getattr(st, f).offset, (st.__name__, f)
     cfg = pirrt.pirrt_config()
     pirrt.pirrt_config_init(C.byref(cfg))
-    assert cfg.nranks == 1 and cfg.epsilon == 0.0 and cfg.flags == 0
+    assert cfg.nranks == 1 and cfg.epsilon == 0.0 and cfg.flags == 0 and cfg.n_goals == 0
 
 
 def test_missing_library_fails_loudly(tmp_path, monkeypatch):

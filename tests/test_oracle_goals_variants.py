@@ -194,3 +194,49 @@ def test_parent_form_prune_off_equals_dijkstra():
     _, g, _, _ = o.state()
     reach = np.isfinite(dist)
     assert np.array_equal(bits(g[reach]), bits(dist[reach]))
+
+
+# --------------------------------------- VALIDATE: duplicates and parent cycles
+
+from oracle import VALIDATE, OracleError  # noqa: E402
+
+
+def test_validate_duplicate_edge_rejected():
+    # a (src,dst) pair stored twice is rejected under
+    # VALIDATE, against the stored graph and inside one batch; state unchanged
+    o = Oracle(flags=VALIDATE)
+    o.append(np.zeros(2), np.array([0, 2], np.int32), np.array([2, 3], np.int32), np.ones(2))
+    before = o.state()
+    for src, dst in (([0], [2]), ([3, 3], [1, 1])):
+        with pytest.raises(OracleError) as ei:
+            o.append(np.zeros(0), np.array(src, np.int32), np.array(dst, np.int32),
+                     np.ones(len(src)))
+        assert ei.value.code == -1
+        for x, y in zip(o.state(), before):
+            assert np.array_equal(x, y)
+    Oracle().append(np.zeros(1), np.array([0, 0], np.int32), np.array([2, 2], np.int32),
+                    np.ones(2))   # accepted without VALIDATE (caller's responsibility)
+
+
+def test_validate_parent_cycle_rejected():
+    # the policy is a tree.  A 3-cycle 2 -> 3 -> 4 -> 2 among
+    # stored edges is rejected by set_policy under VALIDATE (E_CORRUPT)
+    src = np.array([0, 2, 3, 4], np.int32)
+    dst = np.array([2, 3, 4, 2], np.int32)
+    parent = np.array([-1, -1, 4, 2, 3], np.int32)
+    g = np.array([0, np.inf, 1, 1, 1])
+    o = Oracle(flags=VALIDATE)
+    o.append(np.zeros(3), src, dst, np.ones(4))
+    with pytest.raises(OracleError) as ei:
+        o.set_policy(parent, g)
+    assert ei.value.code == -8
+    o2 = Oracle()
+    o2.append(np.zeros(3), src, dst, np.ones(4))
+    o2.set_policy(parent, g)                  # not checked without VALIDATE
+    # a given policy closing a zero-cost 2-cycle passes the g check but not
+    # the cycle check
+    o3 = Oracle(flags=VALIDATE)
+    with pytest.raises(OracleError) as ei:
+        o3.append(np.zeros(2), np.array([3, 2], np.int32), np.array([2, 3], np.int32),
+                  np.zeros(2), parent_new=np.array([3, 2], np.int32), g_new=np.array([1.0, 1.0]))
+    assert ei.value.code == -8 and o3.n == 2
