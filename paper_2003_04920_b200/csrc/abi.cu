@@ -199,6 +199,7 @@ struct pirrt_ctx {
     int wq_tail = -1;                                        // PIRRT_WQ_TAIL (-1: 16 per block)
     int wq_wide = -1;                                        // PIRRT_WQ_WIDE (-1: 10 per block, 0: off)
     int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
+    int wide_tasks = 131072;                                 // PIRRT_WIDE_TASKS: |I| for the wide Improve (0: off)
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
     // goal set G (R4): sorted unique ids incl. x_goal (device copy + host copy)
@@ -447,6 +448,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_WQ_TAIL")) c->wq_tail = std::atoi(w);
     if (const char* w = std::getenv("PIRRT_WQ_WIDE")) c->wq_wide = std::atoi(w);
     if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
+    if (const char* w = std::getenv("PIRRT_WIDE_TASKS")) c->wide_tasks = std::max(0, std::atoi(w));
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -748,12 +750,35 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     } else {
         ExploitArgs a;
         fill_exploit_args(c, a);
+        a.wide_tasks = c->wide_tasks;
+        a.it_base = 1;
         const long long l0 = g_kernel_launches;
         cudaError_t e = launch_exploit(a, c->grid_blocks, c->l2win, s);
-        c->launches += g_kernel_launches - l0;
         if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
-        CU(cudaEventRecord(c->ev1, s));
         if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+        // wide-Improve hand-offs (large improve sets): Improve of iteration
+        // handoff_it at full occupancy, then the loop resumes after it
+        while (c->ctl_host->handoff && !c->ctl_host->abort_at) {
+            const DevCtl& h = *c->ctl_host;
+            ExploitArgs w = a;
+            w.Bsel = h.Bsel_out; w.Bcount = h.Bcount_out; w.old_Bcount = h.old_Bcount_out;
+            w.pending = h.pending_out;
+            w.ev_base = c->ev_next + (unsigned)h.evaluations;
+            const int it = h.handoff_it;
+            CU(cudaMemsetAsync(&c->ctl->handoff, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), s));
+            if ((e = launch_improve_wide(w, it, c->num_sms, s)) == cudaSuccess) {
+                ExploitArgs r = w;
+                r.pending = 0;
+                r.it_base = it;
+                r.resume = 1;
+                e = launch_exploit(r, c->grid_blocks, c->l2win, s);
+            }
+            if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
+            if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+        }
+        c->launches += g_kernel_launches - l0;
+        CU(cudaEventRecord(c->ev1, s));
+        CU(cudaEventSynchronize(c->ev1));
         c->Bsel = c->ctl_host->Bsel_out;
         c->Bcount = c->ctl_host->Bcount_out;
         c->ev_next += (unsigned)c->ctl_host->evaluations;

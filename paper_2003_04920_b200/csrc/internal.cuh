@@ -72,6 +72,11 @@ struct DevCtl {
     unsigned long long dbg_imp[6];    // PIRRT_LEVEL_TRACE Improve timeline
     unsigned long long dbg_lv[32][6]; // PIRRT_LEVEL_TRACE per level: ~min start, max start,
                                       // max work end, max flush end, lead exit, frontier
+    // wide-Improve hand-off: the persistent kernel stopped before the Improve
+    // of iteration handoff_it (|I| >= wide_tasks); the host runs
+    // improve_wide_kernel for it and resumes the loop after that Improve
+    int handoff, handoff_it;
+    unsigned long long t_wide0, t_wide1;   // ~min start / max end of the wide Improve
     // append / set_policy
     int err;                      // bitmask of kErr*
     int nprom;                    // new promising vertices
@@ -133,6 +138,9 @@ struct ExploitArgs {
     const int* goals;
     int n_goals;
     int parent_form;                  // PIRRT_F_PARENT_FORM: P:263 literal test (NEXT-4)
+    int wide_tasks;                   // hand an Improve with |I| >= this to improve_wide_kernel (0: never)
+    int it_base;                      // first PI iteration of this launch (1 = a fresh exploit)
+    int resume;                       // 1: iteration it_base's Improve already ran (wide kernel)
 };
 
 // ---- goal set (reading R4, goal-set form) ----
@@ -185,6 +193,8 @@ cudaError_t launch_shard_evaluate(const ExploitArgs& a, int it, const ShardRec* 
                                   const int* counts, int stride, int nranks, int blocks,
                                   cudaStream_t s);
 int exploit_blocks_per_sm();
+// a3 Improve of iteration `it` as its own high-occupancy launch (large I)
+cudaError_t launch_improve_wide(const ExploitArgs& a, int it, int num_sms, cudaStream_t s);
 int shard_evaluate_blocks_per_sm();
 
 struct AppendArgs {

@@ -334,3 +334,26 @@ def test_split_append_path_parity(P, monkeypatch):
     gpu = P.Context(h_root=r.h_root())
     orc = Oracle(h_root=r.h_root())
     dual_replay(gpu, orc, r, 333)
+
+
+@pytest.mark.parametrize("wide", ["1", "300"])
+@pytest.mark.parametrize("flags", [0, PRUNE_OFF])
+def test_wide_improve_handoff_parity(P, monkeypatch, wide, flags):
+    # every Improve with |I| >= PIRRT_WIDE_TASKS runs as the full-occupancy
+    # launch (hand-off and resume of the persistent loop): same bits, same
+    # counters as the oracle
+    monkeypatch.setenv("PIRRT_WIDE_TASKS", wide)
+    r = gen.rrg(6, 12000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("wide", wide, flags))
+    gpu = P.Context(h_root=r.h_root(), flags=flags)
+    orc = Oracle(h_root=r.h_root(), flags=flags)
+    dual_replay(gpu, orc, r, 1500)
+
+
+def test_wide_improve_cold_solve_and_goal_set(P, monkeypatch):
+    monkeypatch.setenv("PIRRT_WIDE_TASKS", "1000")
+    r = gen.rrg(2, 20000, gen.gamma_star(2), n_boxes=30, seed=gen.seed_of("wide-cold"))
+    ids = np.nonzero(r.h[2:] <= 0.05)[0].astype(np.int32) + 2
+    gpu = P.Context(h_root=r.h_root(), goals=ids)
+    orc = Oracle(h_root=r.h_root())
+    orc.set_goals(ids)
+    dual_replay(gpu, orc, r, r.n)
