@@ -200,6 +200,8 @@ struct pirrt_ctx {
     int wq_wide = -1;                                        // PIRRT_WQ_WIDE (-1: 10 per block, 0: off)
     int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
     int wide_tasks = 131072;                                 // PIRRT_WIDE_TASKS: |I| for the wide Improve (0: off)
+    int kids_min = -1;                                       // PIRRT_KIDS_MIN: |B| for the children index
+                                                             // (-1: 4 n / mean degree; 0: never)
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
     // goal set G (R4): sorted unique ids incl. x_goal (device copy + host copy)
@@ -449,6 +451,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_WQ_WIDE")) c->wq_wide = std::atoi(w);
     if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
     if (const char* w = std::getenv("PIRRT_WIDE_TASKS")) c->wide_tasks = std::max(0, std::atoi(w));
+    if (const char* w = std::getenv("PIRRT_KIDS_MIN")) c->kids_min = std::atoi(w);
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -669,6 +672,16 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;
     a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
     a.parent_form = (c->cfg.flags & PIRRT_F_PARENT_FORM) ? 1 : 0;
+    // children index for large Evaluates: worth it once |B| x mean out-degree
+    // exceeds ~4 n row entries; built in the append scratch (idle during an
+    // exploit): cnt holds 4 (vcap + 1) ints, app_bsum >= kMaxGridBlocks ints
+    const double E = (double)(c->base_edges + c->delta_edges);
+    const double mean_deg = c->n > 0 ? std::max(1.0, E / c->n) : 1.0;
+    a.kids_min = c->kids_min >= 0 ? c->kids_min
+                                  : (int)std::min<double>(INT32_MAX, std::max(4096.0, 4.0 * c->n / mean_deg));
+    a.coff = (int*)c->cnt;
+    a.kids = (int*)c->cnt + (c->vcap + 1);
+    a.kids_bsum = (int*)c->app_bsum;
 }
 
 // Sharded exploit: per PI iteration

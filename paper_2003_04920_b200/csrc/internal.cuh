@@ -141,6 +141,11 @@ struct ExploitArgs {
     int wide_tasks;                   // hand an Improve with |I| >= this to improve_wide_kernel (0: never)
     int it_base;                      // first PI iteration of this launch (1 = a fresh exploit)
     int resume;                       // 1: iteration it_base's Improve already ran (wide kernel)
+    // children index for large Evaluates (build_children): |B| >= kids_min (0: never)
+    int kids_min;
+    int* coff;                        // [n]: after the build row(p) = [p ? coff[p-1] : 0, coff[p])
+    int* kids;                        // [n]
+    int* kids_bsum;                   // [grid blocks] scan partials
 };
 
 // ---- goal set (reading R4, goal-set form) ----

@@ -357,3 +357,29 @@ def test_wide_improve_cold_solve_and_goal_set(P, monkeypatch):
     orc = Oracle(h_root=r.h_root())
     orc.set_goals(ids)
     dual_replay(gpu, orc, r, r.n)
+
+
+@pytest.mark.parametrize("env", [{}, {"PIRRT_BFS": "wq", "PIRRT_WQ_KEEP": "3"},
+                                 {"PIRRT_WQ_TAIL": "0", "PIRRT_WQ_WIDE": "0"},
+                                 {"PIRRT_WIDE_TASKS": "500"}])
+@pytest.mark.parametrize("flags", [0, PRUNE_OFF])
+def test_children_index_evaluate_parity(P, monkeypatch, env, flags):
+    # every Evaluate builds the children index (PIRRT_KIDS_MIN=1) instead of
+    # scanning out-rows: same bits and counters as the oracle
+    monkeypatch.setenv("PIRRT_KIDS_MIN", "1")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    r = gen.rrg(6, 12000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("kids", flags))
+    gpu = P.Context(h_root=r.h_root(), flags=flags)
+    orc = Oracle(h_root=r.h_root(), flags=flags)
+    dual_replay(gpu, orc, r, 900)
+
+
+@pytest.mark.parametrize("gb", [1, 7])
+def test_children_index_small_grids_and_sharded(P, monkeypatch, gb):
+    monkeypatch.setenv("PIRRT_KIDS_MIN", "100")
+    r = gen.rrg(2, 6000, gen.gamma_star(2), n_boxes=20, seed=gen.seed_of("kids-gb", gb))
+    for extra in (0, P.PIRRT_F_SHARDED):
+        gpu = P.Context(h_root=r.h_root(), grid_blocks=gb, flags=extra)
+        orc = Oracle(h_root=r.h_root())
+        dual_replay(gpu, orc, r, 600)
