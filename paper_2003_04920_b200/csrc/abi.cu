@@ -768,6 +768,7 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
         const long long l0 = g_kernel_launches;
         cudaError_t e = launch_exploit(a, c->grid_blocks, c->l2win, s);
         if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
+        CU(cudaEventRecord(c->ev1, s));                  // re-recorded after every resume
         if ((rc = read_ctl(c))) { c->broken = true; return rc; }
         // wide-Improve hand-offs (large improve sets): Improve of iteration
         // handoff_it at full occupancy, then the loop resumes after it
@@ -787,11 +788,10 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
                 e = launch_exploit(r, c->grid_blocks, c->l2win, s);
             }
             if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
+            CU(cudaEventRecord(c->ev1, s));
             if ((rc = read_ctl(c))) { c->broken = true; return rc; }
         }
         c->launches += g_kernel_launches - l0;
-        CU(cudaEventRecord(c->ev1, s));
-        CU(cudaEventSynchronize(c->ev1));
         c->Bsel = c->ctl_host->Bsel_out;
         c->Bcount = c->ctl_host->Bcount_out;
         c->ev_next += (unsigned)c->ctl_host->evaluations;
