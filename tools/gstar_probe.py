@@ -1,0 +1,125 @@
+"""SURVEY.md section 8(d) config 3 at its headline radius gamma*: the 6-D RRG
+(mean degree ~1,100, ~1.1e9 directed edges at 1M vertices).  Reports, for
+n = --n: generation time, the cold solve (S = N: one append + one exploit)
+with its Improve / Evaluate split and algorithmic bandwidth, the per-batch
+exploits of S in --S for the last 10 batches before n (history replayed in
+batches of --pre untimed), and -- if --oracle -- the serial oracle on the
+cold solve (1 core).
+
+    python tools/gstar_probe.py --n 1000000 --out gpurun_out/gstar.json
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+import suite  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--d", type=int, default=6)
+    ap.add_argument("--boxes", type=int, default=20)
+    ap.add_argument("--S", default="4096,65536")
+    ap.add_argument("--pre", type=int, default=131072)
+    ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--out", default="gpurun_out/gstar.json")
+    a = ap.parse_args()
+    import bench
+    peaks = {"hbm_gbs": bench.peaks()[0]}
+    t0 = time.perf_counter()
+    g = gen.rrg(a.d, a.n, gen.gamma_star(a.d), n_boxes=a.boxes,
+                seed=gen.seed_of(f"cfg3_{a.d}d_{a.n}_gammastar_{a.boxes}boxes"))
+    rep = {"d": a.d, "n": a.n, "gamma": "star", "gamma_value": gen.gamma_star(a.d),
+           "boxes": a.boxes, "generate_s": time.perf_counter() - t0,
+           "mean_degree": g.mean_degree, "directed_edges": 2 * g.n_pairs, "isolated": g.n_isolated}
+    print(json.dumps(rep), flush=True)
+    # cold solve
+    ctx, rows = suite.gpu_replay(g, a.n, a.n)
+    st = rows[0][2]
+    bytes_ = st.relaxations * 20 + st.improve_set * 40 + st.eval_scanned * 8 + st.eval_visits * 38
+    rep["cold"] = {"append_ms": rows[0][0], "exploit_ms": rows[0][1], "device_ms": st.device_ms,
+                   "iterations": st.iterations, "evaluations": st.evaluations,
+                   "relaxations": st.relaxations, "improve_ms": st.improve_ms,
+                   "evaluate_ms": st.evaluate_ms,
+                   "improve_GBps_algorithmic": st.relaxations * 20 / (st.improve_ms * 1e-3) / 1e9,
+                   "exploit_GBps_algorithmic": bytes_ / (st.device_ms * 1e-3) / 1e9,
+                   "exploit_frac_hbm": bytes_ / (st.device_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                   "gteps": st.relaxations / (st.device_ms * 1e-3) / 1e9,
+                   "promising": st.promising, "max_level": st.max_level}
+    print(json.dumps(rep["cold"]), flush=True)
+    del ctx
+    import torch
+    torch.cuda.empty_cache()
+    # per batch
+    rep["per_batch"] = {}
+    for S in [int(x) for x in a.S.split(",")]:
+        t_from = a.n - 10 * S
+        ctx, rows = per_batch(g, S, a.pre, t_from, a.n)
+        s = suite.exploit_summary(rows)
+        ex = [r[2] for r in rows if r[2] is not None]
+        s["device_ms_mean"] = float(np.mean([x.device_ms for x in ex])) if ex else None
+        s["improve_ms_mean"] = float(np.mean([x.improve_ms for x in ex])) if ex else None
+        s["evaluate_ms_mean"] = float(np.mean([x.evaluate_ms for x in ex])) if ex else None
+        s["promising_mean"] = float(np.mean([x.promising for x in ex])) if ex else None
+        s["gteps"] = (sum(x.relaxations for x in ex) / (sum(x.device_ms for x in ex) * 1e-3) / 1e9
+                      if ex else None)
+        rep["per_batch"][f"S{S}"] = s
+        print(S, json.dumps(s), flush=True)
+        del ctx
+        torch.cuda.empty_cache()
+    if a.oracle:
+        from oracle import EDGES_UNDIRECTED, Oracle
+        o = Oracle(h_root=g.h_root())
+        s_, d_, c_ = g.batch(2, a.n, directed=False)
+        t0 = time.perf_counter()
+        o.append(g.h[2:a.n], s_, d_, c_, flags=EDGES_UNDIRECTED)
+        t1 = time.perf_counter()
+        ost = o.exploit()
+        t2 = time.perf_counter()
+        rep["cold"]["oracle"] = {"append_ms": 1e3 * (t1 - t0), "exploit_ms": 1e3 * (t2 - t1),
+                                 "iterations": ost.iterations, "relaxations": ost.relaxations,
+                                 "cores": 1}
+        print(json.dumps(rep["cold"]["oracle"]), flush=True)
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    json.dump(rep, open(a.out, "w"), indent=1)
+
+
+def per_batch(g, S, pre, t_from, n_stop):
+    """History up to t_from in batches of `pre` (untimed), then batches of S."""
+    import torch
+    from paper_2003_04920_b200 import pirrt
+    ctx = pirrt.Context(h_root=g.h_root(), stream=torch.cuda.current_stream(),
+                        vertex_capacity=g.n + 1024, edge_capacity=int(2.4 * g.off[-1]) + 4096)
+    a = 2
+    while a < t_from:
+        b = min(t_from, a + pre)
+        s, dd, c = g.batch(a, b, directed=False)
+        if ctx.append(g.h[a:b], s, dd, c, flags=pirrt.PIRRT_F_EDGES_UNDIRECTED) > 0:
+            ctx.exploit()
+        a = b
+    rows = []
+    while a < n_stop:
+        b = min(n_stop, a + S)
+        s, dd, c = g.batch(a, b, directed=False)
+        args = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (g.h[a:b], s, dd, c)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nprom = ctx.append(*args, flags=pirrt.PIRRT_F_EDGES_UNDIRECTED)
+        t1 = time.perf_counter()
+        st = ctx.exploit() if nprom > 0 else None
+        t2 = time.perf_counter()
+        rows.append((1e3 * (t1 - t0), 1e3 * (t2 - t1), st))
+        a = b
+    return ctx, rows
+
+
+if __name__ == "__main__":
+    main()
