@@ -156,6 +156,22 @@ int pirrt_graph_append_batch(pirrt_ctx* ctx, int32_t n_new, const double* h_new,
  * Errors: E_NOCONV after max_iterations Improves (state as left). */
 int pirrt_exploit(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
 
+/* Asynchronous exploit (PAPER.md:565-574:
+ * "asynchronous policy iteration exploitation concurrent with exploration").
+ * pirrt_exploit_async enqueues the same exploit on the context's stream and
+ * returns at once, so the caller's exploration (sampling, collision checks,
+ * building the next batch) runs while the GPU exploits.  pirrt_exploit_wait
+ * completes it and returns its stats and result code (as pirrt_exploit).
+ * Any other call on the context first completes a pending exploit (its
+ * result is kept for the next pirrt_exploit_wait) -- except that
+ * pirrt_graph_append_batch with host inputs first starts their H2D copies
+ * on a side stream, overlapping the running exploit, and only then waits.
+ * Results are identical to pirrt_exploit; Alg. 3's order (append after the
+ * previous Replan) is unchanged.  Sharded contexts run the exploit inside
+ * pirrt_exploit_async.  E_STATE: wait without a started exploit. */
+int pirrt_exploit_async(pirrt_ctx* ctx);
+int pirrt_exploit_wait(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
+
 /* Read-out (host outputs, cap >= pirrt_num_vertices or E_RANGE, nothing written). */
 int pirrt_get_policy(const pirrt_ctx* ctx, pirrt_vid* parent_out, int64_t cap);
 int pirrt_get_costs(const pirrt_ctx* ctx, double* g_out, int64_t cap);

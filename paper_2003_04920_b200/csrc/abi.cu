@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
@@ -207,6 +208,15 @@ struct pirrt_ctx {
     // goal set G (R4): sorted unique ids incl. x_goal (device copy + host copy)
     int* goals = nullptr; int64_t goals_cap = 0;
     std::vector<int> goals_host;
+    // asynchronous exploit (pirrt_exploit_async / pirrt_exploit_wait)
+    bool inflight = false;        // an exploit was launched and not finished
+    ExploitArgs x_args;           // its first launch's arguments (hand-offs reuse them)
+    int x_rc = 0;                 // sharded loop result
+    bool kept = false;            // finished implicitly by another call: result kept
+    int kept_rc = 0;
+    pirrt_exploit_stats kept_stats;
+    cudaStream_t copy_stream = nullptr;   // H2D of the next batch while an exploit runs
+    cudaEvent_t copy_done = nullptr;
 };
 
 namespace {
@@ -329,18 +339,21 @@ void free_all(pirrt_ctx* c) {
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->copy_done) cudaEventDestroy(c->copy_done);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (c->comm && nccl_api()) nccl_api()->commDestroy(c->comm);
 }
 
 template <class T>
 int stage(pirrt_ctx* c, const T* src, int64_t count, bool device, T*& buf, int64_t& cap,
-          const T** out) {
+          const T** out, cudaStream_t s = nullptr) {
     if (count == 0 || src == nullptr) { *out = src; return 0; }
     if (device) { *out = src; return 0; }
+    if (!s) s = c->stream;
     int rc;
-    if ((rc = grow(buf, cap, count, 0, c->stream))) return rc;
-    CU(cudaMemcpyAsync(buf, src, (size_t)count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    if ((rc = grow(buf, cap, count, 0, s))) return rc;
+    CU(cudaMemcpyAsync(buf, src, (size_t)count * sizeof(T), cudaMemcpyHostToDevice, s));
     *out = buf;
     return 0;
 }
@@ -399,8 +412,13 @@ int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
     c->base_edges = E;
     c->obase_edges = E;
     c->delta_edges = 0;
+    // the fold belongs to this append: finish it before returning, so that
+    // it is neither hidden in nor charged to the next call on the stream
+    CU(cudaStreamSynchronize(c->stream));
     return 0;
 }
+
+int complete_pending(pirrt_ctx* c);   // below, with the exploit
 
 }  // namespace
 
@@ -503,7 +521,9 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (cudaMalloc(&c->ctl, sizeof(DevCtl)) != cudaSuccess) return bail(fail(PIRRT_E_NOMEM, "ctl"));
     if (cudaMallocHost(&c->ctl_host, sizeof(DevCtl)) != cudaSuccess)
         return bail(fail(PIRRT_E_NOMEM, "ctl host"));
-    if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
+    if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "events"));
     if (cfg.nranks > 1 || (cfg.flags & PIRRT_F_SHARDED)) {
         NcclApi* api = nccl_api();
@@ -575,8 +595,28 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     const bool dev = (flags & PIRRT_F_DEVICE_PTRS) != 0;
     const bool undirected = (flags & PIRRT_F_EDGES_UNDIRECTED) != 0;
     const int64_t m_dir = undirected ? 2 * n_edges : n_edges;
-    const int n_old = c->n, n_all = c->n + n_new;
     cudaStream_t s = c->stream;
+    // inputs.  While an exploit started by pirrt_exploit_async still runs,
+    // host inputs are copied on the side stream so that the H2D overlaps it
+    // (SURVEY.md section 8(f) NEXT-1); the append itself waits for it.
+    const double *d_h = nullptr, *d_g = nullptr, *d_cost = nullptr;
+    const int *d_parent = nullptr, *d_src = nullptr, *d_dst = nullptr;
+    const bool early = c->inflight && !dev;
+    auto stage_all = [&](cudaStream_t ss) -> int {
+        int r;
+        if ((r = stage(c, h_new, n_new, dev, c->s_h, c->s_h_cap, &d_h, ss))) return r;
+        if ((r = stage(c, parent_new, n_new, dev, c->s_parent, c->s_parent_cap, &d_parent, ss))) return r;
+        if ((r = stage(c, g_new, n_new, dev, c->s_g, c->s_g_cap, &d_g, ss))) return r;
+        if ((r = stage(c, src, n_edges, dev, c->s_src, c->s_src_cap, &d_src, ss))) return r;
+        if ((r = stage(c, dst, n_edges, dev, c->s_dst, c->s_dst_cap, &d_dst, ss))) return r;
+        return stage(c, cost, n_edges, dev, c->s_cost, c->s_cost_cap, &d_cost, ss);
+    };
+    if (early) {
+        if ((rc = stage_all(c->copy_stream))) return rc;
+        CU(cudaEventRecord(c->copy_done, c->copy_stream));
+    }
+    if ((rc = complete_pending(c))) return rc;
+    const int n_old = c->n, n_all = c->n + n_new;
     // capacity (growth does not change state)
     if ((rc = ensure_vertices(c, n_all))) return rc;
     const int nb = 1 - c->cur;
@@ -584,15 +624,8 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     if ((rc = grow(c->didx[nb], c->didx_cap[nb], dneed, 0, s))) return rc;
     if ((rc = grow(c->dcost[nb], c->dcost_cap[nb], dneed, 0, s))) return rc;
     if ((rc = grow(c->odidx[nb], c->odidx_cap[nb], dneed, 0, s))) return rc;
-    // inputs
-    const double *d_h = nullptr, *d_g = nullptr, *d_cost = nullptr;
-    const int *d_parent = nullptr, *d_src = nullptr, *d_dst = nullptr;
-    if ((rc = stage(c, h_new, n_new, dev, c->s_h, c->s_h_cap, &d_h))) return rc;
-    if ((rc = stage(c, parent_new, n_new, dev, c->s_parent, c->s_parent_cap, &d_parent))) return rc;
-    if ((rc = stage(c, g_new, n_new, dev, c->s_g, c->s_g_cap, &d_g))) return rc;
-    if ((rc = stage(c, src, n_edges, dev, c->s_src, c->s_src_cap, &d_src))) return rc;
-    if ((rc = stage(c, dst, n_edges, dev, c->s_dst, c->s_dst_cap, &d_dst))) return rc;
-    if ((rc = stage(c, cost, n_edges, dev, c->s_cost, c->s_cost_cap, &d_cost))) return rc;
+    if (early) CU(cudaStreamWaitEvent(s, c->copy_done, 0));
+    else if ((rc = stage_all(s))) return rc;
     CU(cudaMemsetAsync(&c->ctl->err, 0, 4 * sizeof(int), s));   // err, nprom, sweeps
     CU(cudaMemsetAsync(&c->ctl->sweep_changed[0], 0, 2 * sizeof(int), s));
     AppendArgs a;
@@ -747,39 +780,62 @@ static int exploit_sharded(pirrt_ctx* c) {
     return 0;
 }
 
-int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
-    if (!c) return fail(PIRRT_E_INVAL, "exploit: NULL context");
-    int rc;
-    if ((rc = set_device(c))) return rc;
+}  // extern "C"
+
+namespace {
+
+// Exploit, split for the asynchronous form:
+// exploit_launch enqueues the first persistent launch (single GPU) and
+// returns; exploit_finish reads the control block, serves wide-Improve
+// hand-offs and fills the stats.  The sharded loop is host-driven (NCCL
+// between the phases), so it runs entirely inside exploit_launch.
+int exploit_launch(pirrt_ctx* c) {
     cudaStream_t s = c->stream;
     CU(cudaMemsetAsync(c->ctl, 0, offsetof(DevCtl, err), s));
     CU(cudaEventRecord(c->ev0, s));
-    int xrc = 0;
+    c->x_rc = 0;
     if (c->sharded) {
-        xrc = exploit_sharded(c);
-        if (xrc != 0 && xrc != PIRRT_E_NOCONV) { c->broken = true; return xrc; }
+        c->x_rc = exploit_sharded(c);
+        if (c->x_rc != 0 && c->x_rc != PIRRT_E_NOCONV) { c->broken = true; return c->x_rc; }
         CU(cudaEventRecord(c->ev1, s));
-        if ((rc = read_ctl(c))) { c->broken = true; return rc; }
-    } else {
-        ExploitArgs a;
-        fill_exploit_args(c, a);
-        a.wide_tasks = c->wide_tasks;
-        a.it_base = 1;
-        const long long l0 = g_kernel_launches;
-        cudaError_t e = launch_exploit(a, c->grid_blocks, c->l2win, s);
-        if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
-        CU(cudaEventRecord(c->ev1, s));                  // re-recorded after every resume
-        if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+        return 0;
+    }
+    fill_exploit_args(c, c->x_args);
+    c->x_args.wide_tasks = c->wide_tasks;
+    c->x_args.it_base = 1;
+    const long long l0 = g_kernel_launches;
+    cudaError_t e = launch_exploit(c->x_args, c->grid_blocks, c->l2win, s);
+    c->launches += g_kernel_launches - l0;
+    if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
+    CU(cudaEventRecord(c->ev1, s));                      // re-recorded after every resume
+    return 0;
+}
+
+int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
+    cudaStream_t s = c->stream;
+    int rc;
+    const bool dbg = std::getenv("PIRRT_DEBUG_HOST") != nullptr;
+    auto now_us = []() {
+        return std::chrono::duration<double, std::micro>(
+                   std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t_in = dbg ? now_us() : 0.0;
+    if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+    if (dbg) std::fprintf(stderr, "pirrt host: first launch done +%.1f us (handoff=%d it=%d)\n",
+                          now_us() - t_in, c->ctl_host->handoff, c->ctl_host->handoff_it);
+    if (!c->sharded) {
         // wide-Improve hand-offs (large improve sets): Improve of iteration
         // handoff_it at full occupancy, then the loop resumes after it
+        const long long l0 = g_kernel_launches;
         while (c->ctl_host->handoff && !c->ctl_host->abort_at) {
             const DevCtl& h = *c->ctl_host;
-            ExploitArgs w = a;
+            ExploitArgs w = c->x_args;
             w.Bsel = h.Bsel_out; w.Bcount = h.Bcount_out; w.old_Bcount = h.old_Bcount_out;
             w.pending = h.pending_out;
             w.ev_base = c->ev_next + (unsigned)h.evaluations;
             const int it = h.handoff_it;
             CU(cudaMemsetAsync(&c->ctl->handoff, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), s));
+            cudaError_t e;
             if ((e = launch_improve_wide(w, it, c->num_sms, s)) == cudaSuccess) {
                 ExploitArgs r = w;
                 r.pending = 0;
@@ -790,6 +846,10 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
             if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
             CU(cudaEventRecord(c->ev1, s));
             if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+            if (dbg) std::fprintf(stderr, "pirrt host: wide Improve it=%d + resume done +%.1f us "
+                                  "(wide span %.1f us, next handoff=%d)\n", it, now_us() - t_in,
+                                  (c->ctl_host->t_wide1 - ~c->ctl_host->t_wide0) * 1e-3,
+                                  c->ctl_host->handoff);
         }
         c->launches += g_kernel_launches - l0;
         c->Bsel = c->ctl_host->Bsel_out;
@@ -821,9 +881,59 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
         c->broken = true;
         return fail(PIRRT_E_STATE, "exploit: watchdog fired (PIRRT_WATCHDOG_MS); context unusable");
     }
-    if (xrc == PIRRT_E_NOCONV || h.status == PIRRT_E_NOCONV)
+    if (c->x_rc == PIRRT_E_NOCONV || h.status == PIRRT_E_NOCONV)
         return fail(PIRRT_E_NOCONV, "exploit: iteration cap exceeded");
     return PIRRT_OK;
+}
+
+// Complete an exploit started by pirrt_exploit_async before any other call
+// touches the context; its result is kept for pirrt_exploit_wait.  Returns
+// nonzero only if the context became unusable.
+int complete_pending(pirrt_ctx* c) {
+    if (!c->inflight) return 0;
+    c->inflight = false;
+    c->kept_rc = exploit_finish(c, &c->kept_stats);
+    c->kept = true;
+    return c->broken ? c->kept_rc : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
+    if (!c) return fail(PIRRT_E_INVAL, "exploit: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
+    c->kept = false;
+    if ((rc = exploit_launch(c))) return rc;
+    return exploit_finish(c, st);
+}
+
+int pirrt_exploit_async(pirrt_ctx* c) {
+    if (!c) return fail(PIRRT_E_INVAL, "exploit_async: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
+    c->kept = false;
+    if ((rc = exploit_launch(c))) return rc;
+    c->inflight = true;
+    return PIRRT_OK;
+}
+
+int pirrt_exploit_wait(pirrt_ctx* c, pirrt_exploit_stats* st) {
+    if (!c) return fail(PIRRT_E_INVAL, "exploit_wait: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if (c->inflight) {
+        c->inflight = false;
+        return exploit_finish(c, st);
+    }
+    if (!c->kept) return fail(PIRRT_E_STATE, "exploit_wait: no exploit was started");
+    c->kept = false;
+    if (st) *st = c->kept_stats;
+    return c->kept_rc == PIRRT_OK ? PIRRT_OK : fail(c->kept_rc, "exploit: failed (reported late)");
 }
 
 int pirrt_nccl_unique_id(void* out, int64_t cap) {
@@ -841,6 +951,7 @@ static int get_array(const pirrt_ctx* c, void* out, const void* dsrc, size_t ele
     if (!c || !out) return fail(PIRRT_E_INVAL, std::string(what) + ": NULL argument");
     int rc;
     if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(const_cast<pirrt_ctx*>(c)))) return rc;
     if (cap < c->n) return fail(PIRRT_E_RANGE, std::string(what) + ": capacity too small");
     CU(cudaMemcpyAsync(out, dsrc, (size_t)c->n * elem, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -866,6 +977,7 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
     if (!c) return fail(PIRRT_E_INVAL, "best_path: NULL context");
     int rc;
     if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
     cudaStream_t s = c->stream;
     // one small read-back (header + the first kHead entries); a second copy
     // only for paths longer than that
@@ -910,6 +1022,7 @@ int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, con
     if (!parent || !g) return fail(PIRRT_E_INVAL, "set_policy: NULL array");
     int rc;
     if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
     cudaStream_t s = c->stream;
     const int n = c->n;
     const int* d_parent;
@@ -977,6 +1090,7 @@ extern "C" int pirrt_debug_blist(const pirrt_ctx* c, int32_t* out, int64_t cap, 
     if (!c || !out || !count) return fail(PIRRT_E_INVAL, "debug_blist: NULL");
     int rc;
     if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(const_cast<pirrt_ctx*>(c)))) return rc;
     *count = c->Bcount;
     if (cap < c->Bcount + 1) return fail(PIRRT_E_RANGE, "debug_blist: capacity");
     CU(cudaMemcpyAsync(out, c->Bq[c->Bsel], (size_t)(c->Bcount + 1) * sizeof(int),

@@ -42,8 +42,8 @@ NCCL_UNIQUE_ID_BYTES = 128
 # every symbol include/pirrt.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "pirrt_config_init", "pirrt_create", "pirrt_destroy", "pirrt_graph_append_batch",
-    "pirrt_exploit", "pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
-    "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
+    "pirrt_exploit", "pirrt_exploit_async", "pirrt_exploit_wait", "pirrt_get_policy",
+    "pirrt_get_costs", "pirrt_get_promising", "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
     "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id",
     # include/pirrt_bench.h (measurement helpers)
     "pirrt_bench_rows", "pirrt_bench_relax", "pirrt_bench_gather",
@@ -103,6 +103,8 @@ def _load():
     lib.pirrt_graph_append_batch.argtypes = [P, C.c_int32, P, P, P, C.c_int64, P, P, P,
                                              C.c_uint32, P]
     lib.pirrt_exploit.argtypes = [P, C.POINTER(pirrt_exploit_stats)]
+    lib.pirrt_exploit_async.argtypes = [P]
+    lib.pirrt_exploit_wait.argtypes = [P, C.POINTER(pirrt_exploit_stats)]
     for f in ("pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
               "pirrt_get_parent_costs"):
         getattr(lib, f).argtypes = [P, P, C.c_int64]
@@ -130,6 +132,8 @@ pirrt_create = _lib.pirrt_create
 pirrt_destroy = _lib.pirrt_destroy
 pirrt_graph_append_batch = _lib.pirrt_graph_append_batch
 pirrt_exploit = _lib.pirrt_exploit
+pirrt_exploit_async = _lib.pirrt_exploit_async
+pirrt_exploit_wait = _lib.pirrt_exploit_wait
 pirrt_get_policy = _lib.pirrt_get_policy
 pirrt_get_costs = _lib.pirrt_get_costs
 pirrt_get_promising = _lib.pirrt_get_promising
@@ -288,6 +292,16 @@ class Context:
     def exploit(self) -> ExploitStats:
         st = pirrt_exploit_stats()
         _check(pirrt_exploit(self._h, C.byref(st)))
+        return ExploitStats(*(getattr(st, f[0]) for f in pirrt_exploit_stats._fields_))
+
+    def exploit_async(self) -> None:
+        """pirrt_exploit_async: start the exploit and return at once."""
+        _check(pirrt_exploit_async(self._h))
+
+    def exploit_wait(self) -> ExploitStats:
+        """pirrt_exploit_wait: complete the started exploit."""
+        st = pirrt_exploit_stats()
+        _check(pirrt_exploit_wait(self._h, C.byref(st)))
         return ExploitStats(*(getattr(st, f[0]) for f in pirrt_exploit_stats._fields_))
 
     def _get(self, fn, dtype):

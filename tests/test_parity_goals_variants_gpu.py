@@ -190,3 +190,47 @@ def test_validate_cycles_rejected_like_oracle(P):
         ctx.set_policy(parent, g)
     assert_same_stats(gl.exploit(), ol.exploit())
     assert_same_state(gl, ol)
+
+
+# ------------------------------------- asynchronous exploit (NEXT-1)
+
+@pytest.mark.parametrize("d,n,S", [(2, 4000, 37), (6, 20000, 1500)])
+def test_async_exploit_pipelined_replay(P, d, n, S):
+    # Alg. 3 with the exploit of batch k running while batch k+1 is staged
+    # (its H2D on the side stream): same bits and counters as the oracle
+    from paper_2003_04920_b200.berrt import EDGES_UNDIRECTED, batches
+    gamma = gen.gamma_star(d) if d == 2 else gen.gamma_k(d)
+    r = gen.rrg(d, n, gamma, n_boxes=15, seed=gen.seed_of("async-exploit", d))
+    gpu, orc = P.Context(h_root=r.h_root()), Oracle(h_root=r.h_root())
+    started = False
+    for k, (a, b) in enumerate(batches(r.n, S)):
+        src, dst, cost = r.batch(a, b, directed=False)
+        h = np.ascontiguousarray(r.h[a:b])
+        pg = gpu.append(h, src, dst, cost, flags=EDGES_UNDIRECTED)   # overlaps the running exploit
+        if started:
+            assert_same_stats(gpu.exploit_wait(), orc_stats, f"batch {k}")
+            started = False
+        po = orc.append(h, src, dst, cost, flags=EDGES_UNDIRECTED)
+        assert pg == po
+        if po > 0:
+            orc_stats = orc.exploit()
+            gpu.exploit_async()
+            started = True
+            if k % 7 == 0:                 # a read-out completes the pending exploit
+                assert_same_state(gpu, orc, f"batch {k}")
+    if started:
+        assert_same_stats(gpu.exploit_wait(), orc_stats, "last")
+    gpu.exploit_async()
+    assert_same_stats(gpu.exploit_wait(), orc.exploit(), "final")
+    assert_same_state(gpu, orc, "final")
+
+
+def test_async_exploit_wait_without_start(P):
+    gpu = P.Context()
+    with pytest.raises(P.PirrtError) as ei:
+        gpu.exploit_wait()
+    assert ei.value.code == P.PIRRT_E_STATE
+    gpu.exploit_async()
+    gpu.exploit_wait()
+    with pytest.raises(P.PirrtError):
+        gpu.exploit_wait()

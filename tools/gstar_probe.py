@@ -30,17 +30,33 @@ def main():
     ap.add_argument("--S", default="4096,65536")
     ap.add_argument("--pre", type=int, default=131072)
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--cache", default="", help="npz graph cache (written if missing)")
+    ap.add_argument("--skip-batches", action="store_true")
     ap.add_argument("--out", default="gpurun_out/gstar.json")
     a = ap.parse_args()
     import bench
     peaks = {"hbm_gbs": bench.peaks()[0]}
     t0 = time.perf_counter()
-    g = gen.rrg(a.d, a.n, gen.gamma_star(a.d), n_boxes=a.boxes,
-                seed=gen.seed_of(f"cfg3_{a.d}d_{a.n}_gammastar_{a.boxes}boxes"))
+    tag = f"cfg3_{a.d}d_{a.n}_gammastar_{a.boxes}boxes"
+    g, _ = suite.graph(a.d, a.n, gen.gamma_star(a.d), a.boxes, tag, a.cache)
+    if a.cache and not os.path.exists(a.cache):
+        np.savez(a.cache, points=g.points, boxes=g.boxes, h=g.h, off=g.off, nbr=g.nbr, cost=g.cost)
     rep = {"d": a.d, "n": a.n, "gamma": "star", "gamma_value": gen.gamma_star(a.d),
            "boxes": a.boxes, "generate_s": time.perf_counter() - t0,
            "mean_degree": g.mean_degree, "directed_edges": 2 * g.n_pairs, "isolated": g.n_isolated}
     print(json.dumps(rep), flush=True)
+    # warm-up: the first exploit of a process pays one-time costs (module
+    # load, L2 persistence setup), not part of the measurement
+    w = gen.rrg(a.d, 3000, gen.gamma_k(a.d), n_boxes=2, seed=1)
+    wt = os.environ.get("PIRRT_WIDE_TASKS")
+    os.environ["PIRRT_WIDE_TASKS"] = "1"                 # load the wide Improve too
+    wctx, _ = suite.gpu_replay(w, 3000, 3000)
+    if wt is None:
+        del os.environ["PIRRT_WIDE_TASKS"]
+    else:
+        os.environ["PIRRT_WIDE_TASKS"] = wt
+    wctx, _ = suite.gpu_replay(w, 500, 3000)
+    del wctx
     # cold solve
     ctx, rows = suite.gpu_replay(g, a.n, a.n)
     st = rows[0][2]
@@ -60,7 +76,7 @@ def main():
     torch.cuda.empty_cache()
     # per batch
     rep["per_batch"] = {}
-    for S in [int(x) for x in a.S.split(",")]:
+    for S in ([] if a.skip_batches else [int(x) for x in a.S.split(",")]):
         t_from = a.n - 10 * S
         ctx, rows = per_batch(g, S, a.pre, t_from, a.n)
         s = suite.exploit_summary(rows)
