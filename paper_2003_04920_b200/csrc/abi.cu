@@ -602,6 +602,13 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     const double *d_h = nullptr, *d_g = nullptr, *d_cost = nullptr;
     const int *d_parent = nullptr, *d_src = nullptr, *d_dst = nullptr;
     const bool early = c->inflight && !dev;
+    const bool dbg = std::getenv("PIRRT_DEBUG_HOST") != nullptr;
+    auto now_us = []() {
+        return std::chrono::duration<double, std::micro>(
+                   std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t_in = dbg ? now_us() : 0.0;
+    double t_staged = 0.0, t_pending = 0.0;
     auto stage_all = [&](cudaStream_t ss) -> int {
         int r;
         if ((r = stage(c, h_new, n_new, dev, c->s_h, c->s_h_cap, &d_h, ss))) return r;
@@ -615,7 +622,9 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
         if ((rc = stage_all(c->copy_stream))) return rc;
         CU(cudaEventRecord(c->copy_done, c->copy_stream));
     }
+    if (dbg) t_staged = now_us();
     if ((rc = complete_pending(c))) return rc;
+    if (dbg) t_pending = now_us();
     const int n_old = c->n, n_all = c->n + n_new;
     // capacity (growth does not change state)
     if ((rc = ensure_vertices(c, n_all))) return rc;
@@ -662,6 +671,9 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     c->launches += g_kernel_launches - l0;
     if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("append: ") + cudaGetErrorString(e)); }
     if ((rc = read_ctl(c))) { c->broken = true; return rc; }
+    if (dbg) std::fprintf(stderr, "pirrt host: append m=%lld %s: early-staged +%.1f, pending done +%.1f, "
+                          "kernel done +%.1f us\n", (long long)n_edges, dev ? "device" : "host",
+                          t_staged ? t_staged - t_in : 0.0, t_pending - t_in, now_us() - t_in);
     const int err = c->ctl_host->err;
     if (err) {
         int code = (err & (kErrRange)) ? PIRRT_E_RANGE
@@ -752,7 +764,12 @@ static int exploit_sharded(pirrt_ctx* c) {
         CU(cudaMemsetAsync(&c->ctl->it[it & 1], 0, sizeof(IterCtl), s));
         CU(cudaMemsetAsync(c->rec_counts, 0, sizeof(int), s));
         a.Bsel = Bsel; a.Bcount = Bc; a.old_Bcount = old_Bc; a.pending = pending; a.ev_base = ev;
-        CU(launch_shard_improve(a, it, c->shard_blocks, s));
+        const int64_t tasks = a.prune_off ? (int64_t)c->n - 1 : (int64_t)Bc + a.n_goals;
+        if (c->wide_tasks > 0 && tasks >= c->wide_tasks) {
+            CU(launch_improve_wide(a, it, c->num_sms, s));   // large I: full-occupancy Improve
+        } else {
+            CU(launch_shard_improve(a, it, c->shard_blocks, s));
+        }
         c->launches += 1;
         NC(api->allGather(c->rec_counts, c->rec_counts + 1, 1, ncclInt32, c->comm, s));
         CU(cudaMemcpyAsync(counts.data(), c->rec_counts, sizeof(int) * (c->nranks + 1),

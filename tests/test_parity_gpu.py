@@ -383,3 +383,13 @@ def test_children_index_small_grids_and_sharded(P, monkeypatch, gb):
         gpu = P.Context(h_root=r.h_root(), grid_blocks=gb, flags=extra)
         orc = Oracle(h_root=r.h_root())
         dual_replay(gpu, orc, r, 600)
+
+
+def test_sharded_loop_wide_improve(P, monkeypatch):
+    # the sharded loop's Improve as the full-occupancy launch (records path)
+    monkeypatch.setenv("PIRRT_WIDE_TASKS", "200")
+    r = gen.rrg(6, 12000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("shard-wide"))
+    for flags in (0, PRUNE_OFF):
+        gpu = P.Context(h_root=r.h_root(), flags=flags | P.PIRRT_F_SHARDED)
+        orc = Oracle(h_root=r.h_root(), flags=flags)
+        dual_replay(gpu, orc, r, 2000)
