@@ -35,6 +35,8 @@ def _load():
         lib.gen_sizes.argtypes = [C.c_void_p] + [C.c_void_p] * 4
         lib.gen_copy.argtypes = [C.c_void_p] + [C.c_void_p] * 6
         lib.gen_free.argtypes = [C.c_void_p]
+        lib.gen_points.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_double, C.c_double,
+                                   C.c_uint64, C.c_void_p, C.c_void_p]
         _lib = lib
     return _lib
 
@@ -128,6 +130,20 @@ def rrg(d: int, n: int, gamma: float, n_boxes: int = 0, side=(0.05, 0.3), seed: 
         return RRG(d, nn, gamma, pts, boxes, hv, off, nbr, cost, int(sz[2]), int(sz[3]))
     finally:
         lib.gen_free(h)
+
+
+def points(d: int, n: int, n_boxes: int = 0, side=(0.05, 0.3), seed: int = 1):
+    """Only the samples of rrg(...) with the same arguments: (points (n, d),
+    boxes (n_boxes, 2, d)) -- for the device-side Extend, which builds the
+    edges itself."""
+    lib = _load()
+    pts = np.empty((n, d), np.float64)
+    boxes = np.empty((max(n_boxes, 0), 2, d), np.float64)
+    rc = lib.gen_points(int(d), int(n), int(n_boxes), float(side[0]), float(side[1]),
+                        C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), boxes.ctypes.data, pts.ctypes.data)
+    if rc != 0:
+        raise ValueError("gen_points: bad arguments")
+    return pts, boxes
 
 
 # ---------------------------------------------------------------- tiny graphs

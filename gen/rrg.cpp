@@ -262,6 +262,38 @@ void* gen_rrg(int d, int64_t n, double gamma, int n_boxes, double side_lo,
     return G;
 }
 
+// Only the sampling half of gen_rrg (same RNG stream: the same boxes and
+// points), for a planner that builds its edges on the device
+// (pirrt_extend_batch).  boxes [n_boxes][2][d], pts [n][d].
+int gen_points(int d, int64_t n, int n_boxes, double side_lo, double side_hi, uint64_t seed,
+               double* boxes, double* pts) {
+    if (d < 1 || d > 16 || n < 2) return -1;
+    SplitMix64 rng(seed);
+    std::vector<double> xi(d, 0.1), xg(d, 0.9);
+    for (int bI = 0; bI < n_boxes; ++bI) {
+        double* box = &boxes[(size_t)bI * 2 * d];
+        for (int tries = 0; tries < 100000; ++tries) {
+            for (int k = 0; k < d; ++k) {
+                double side = side_lo + (side_hi - side_lo) * rng.uniform();
+                double lo = (1.0 - side) * rng.uniform();
+                box[k] = lo; box[d + k] = lo + side;
+            }
+            if (!in_box(xi.data(), box, d) && !in_box(xg.data(), box, d)) break;
+        }
+    }
+    for (int k = 0; k < d; ++k) { pts[k] = xi[k]; pts[d + k] = xg[k]; }
+    for (int64_t i = 2; i < n; ++i) {
+        double* p = &pts[(size_t)i * d];
+        for (int tries = 0; ; ++tries) {
+            for (int k = 0; k < d; ++k) p[k] = rng.uniform();
+            bool inside = false;
+            for (int bI = 0; bI < n_boxes && !inside; ++bI) inside = in_box(p, &boxes[(size_t)bI * 2 * d], d);
+            if (!inside || tries > 1000000) break;
+        }
+    }
+    return 0;
+}
+
 void gen_sizes(void* h, int64_t* n, int64_t* n_pairs, int64_t* n_isolated,
                int64_t* n_candidates) {
     Gen* G = (Gen*)h;

@@ -205,6 +205,36 @@ int64_t pirrt_num_edges(const pirrt_ctx* ctx);   /* directed edges stored */
  * pirrt_nccl_unique_id writes the 128-byte ncclUniqueId (call on one rank). */
 int pirrt_nccl_unique_id(void* out, int64_t cap);
 
+/* Device-side Extend: the
+ * graph-growth half of a BE-RRT# batch on the GPU, so that a batch crosses
+ * PCIe as n_new sample points instead of ~2 x n_new x degree edge triples.
+ *
+ * pirrt_set_world: the configuration space [0,1]^d with n_boxes axis-aligned
+ * obstacle boxes (boxes[b][0][k] = lower, boxes[b][1][k] = upper corner,
+ * row-major [n_boxes][2][d]), x_init / x_goal (the points of vertices 0 and
+ * 1) and the connection constant gamma.  Call once, before the first append
+ * (E_STATE otherwise); afterwards the context grows only through
+ * pirrt_extend_batch (a plain append returns E_STATE).
+ *
+ * pirrt_extend_batch: points [n_new][d] (host, or device with
+ * PIRRT_F_DEVICE_PTRS; the caller samples them, e.g. uniformly outside the
+ * boxes) become vertices [n, n + n_new) in order.  New vertex i connects to
+ * every earlier j < i with |x_i - x_j| <= r(i + 1), r(m) = gamma (ln m /
+ * m)^(1/d), whose segment misses every box (closed boxes, slab test); cost =
+ * |x_i - x_j| (fp64, squared differences summed in coordinate order), both
+ * directions; h(i) = |x_i - x_goal|.  The triples are built on the device
+ * (uniform grid, one warp per new vertex) and appended as by
+ * pirrt_graph_append_batch with PIRRT_F_EDGES_UNDIRECTED (local relaxation,
+ * promising test; flags may add PIRRT_F_VALIDATE).  *n_edges_out (nullable)
+ * = undirected pairs created.  Errors as the append; state unchanged.
+ *
+ * pirrt_get_points: the points of all n vertices ([n][d], host). */
+int pirrt_set_world(pirrt_ctx* ctx, int32_t d, int32_t n_boxes, const double* boxes,
+                    const double* x_init, const double* x_goal, double gamma);
+int pirrt_extend_batch(pirrt_ctx* ctx, int32_t n_new, const double* points, uint32_t flags,
+                       int32_t* n_new_promising, int64_t* n_edges_out);
+int pirrt_get_points(const pirrt_ctx* ctx, double* points_out, int64_t cap);
+
 /* Number of CUDA kernels this context has launched so far (diagnostics). */
 int64_t pirrt_kernel_launches(const pirrt_ctx* ctx);
 const char* pirrt_last_error(void);              /* thread-local; valid until the next call */

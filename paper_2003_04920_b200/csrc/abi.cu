@@ -217,6 +217,25 @@ struct pirrt_ctx {
     pirrt_exploit_stats kept_stats;
     cudaStream_t copy_stream = nullptr;   // H2D of the next batch while an exploit runs
     cudaEvent_t copy_done = nullptr;
+    // device-side Extend (pirrt_set_world / pirrt_extend_batch)
+    int w_d = 0, w_nboxes = 0;
+    double w_gamma = 0.0;
+    double* w_boxes = nullptr; int64_t w_boxes_cap = 0;
+    double* w_goal = nullptr; int64_t w_goal_cap = 0;
+    double* pts = nullptr; int64_t pts_cap = 0;           // [n][d] every vertex's point
+    int* x_cell = nullptr; int64_t x_cell_cap = 0;
+    int* x_cpts = nullptr; int64_t x_cpts_cap = 0;
+    long long* x_ccnt = nullptr; int64_t x_ccnt_cap = 0;
+    long long* x_cstart = nullptr; int64_t x_cstart_cap = 0;
+    long long* x_tmp = nullptr; int64_t x_tmp_cap = 0;
+    double* x_R = nullptr; int64_t x_R_cap = 0;
+    double* x_h = nullptr; int64_t x_h_cap = 0;
+    long long* x_ecnt = nullptr; int64_t x_ecnt_cap = 0;
+    long long* x_eoff = nullptr; int64_t x_eoff_cap = 0;
+    int* x_src = nullptr; int64_t x_src_cap = 0;
+    int* x_dst = nullptr; int64_t x_dst_cap = 0;
+    double* x_cost = nullptr; int64_t x_cost_cap = 0;
+    bool in_extend = false;       // the append is pirrt_extend_batch's own
 };
 
 namespace {
@@ -333,7 +352,9 @@ void free_all(pirrt_ctx* c) {
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
                     c->qv, c->qg, c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
-                    c->rec_local, c->rec_all, c->rec_counts, c->app_bsum, c->goals};
+                    c->rec_local, c->rec_all, c->rec_counts, c->app_bsum, c->goals,
+                    c->w_boxes, c->w_goal, c->pts, c->x_cell, c->x_cpts, c->x_ccnt, c->x_cstart,
+                    c->x_tmp, c->x_R, c->x_h, c->x_ecnt, c->x_eoff, c->x_src, c->x_dst, c->x_cost};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
@@ -592,6 +613,8 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     if (n_new > 0 && !h_new) return fail(PIRRT_E_INVAL, "append: h_new is NULL");
     if (n_edges > 0 && (!src || !dst || !cost)) return fail(PIRRT_E_INVAL, "append: NULL edge array");
     if ((int64_t)c->n + n_new > INT32_MAX - 1) return fail(PIRRT_E_RANGE, "append: too many vertices");
+    if (c->w_d != 0 && !c->in_extend && n_new > 0)
+        return fail(PIRRT_E_STATE, "append: a context with a world grows through pirrt_extend_batch");
     const bool dev = (flags & PIRRT_F_DEVICE_PTRS) != 0;
     const bool undirected = (flags & PIRRT_F_EDGES_UNDIRECTED) != 0;
     const int64_t m_dir = undirected ? 2 * n_edges : n_edges;
@@ -1097,6 +1120,123 @@ int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, con
     CU(cudaMemcpyAsync(&bc, cnt_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     c->Bcount = bc;
+    return PIRRT_OK;
+}
+
+
+// ---- device-side Extend
+
+int pirrt_set_world(pirrt_ctx* c, int32_t d, int32_t n_boxes, const double* boxes,
+                    const double* x_init, const double* x_goal, double gamma) {
+    if (!c) return fail(PIRRT_E_INVAL, "set_world: NULL context");
+    if (d < 1 || d > 16 || n_boxes < 0 || (n_boxes > 0 && !boxes) || !x_init || !x_goal ||
+        !(gamma > 0.0) || std::isinf(gamma))
+        return fail(PIRRT_E_INVAL, "set_world: bad arguments");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
+    if (c->n != 2) return fail(PIRRT_E_STATE, "set_world: must precede the first append");
+    for (int64_t k = 0; k < (int64_t)n_boxes * 2 * d; ++k)
+        if (!std::isfinite(boxes[k])) return fail(PIRRT_E_INVAL, "set_world: non-finite box");
+    for (int k = 0; k < d; ++k)
+        if (!std::isfinite(x_init[k]) || !std::isfinite(x_goal[k]))
+            return fail(PIRRT_E_INVAL, "set_world: non-finite point");
+    cudaStream_t s = c->stream;
+    if ((rc = grow(c->w_boxes, c->w_boxes_cap, std::max<int64_t>(1, (int64_t)n_boxes * 2 * d), 0, s))) return rc;
+    if ((rc = grow(c->w_goal, c->w_goal_cap, d, 0, s))) return rc;
+    if ((rc = grow(c->pts, c->pts_cap, std::max<int64_t>(2, c->vcap) * d, 0, s))) return rc;
+    if (n_boxes) CU(cudaMemcpyAsync(c->w_boxes, boxes, sizeof(double) * n_boxes * 2 * d, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(c->w_goal, x_goal, sizeof(double) * d, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(c->pts, x_init, sizeof(double) * d, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(c->pts + d, x_goal, sizeof(double) * d, cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+    c->w_d = d; c->w_nboxes = n_boxes; c->w_gamma = gamma;
+    return PIRRT_OK;
+}
+
+int pirrt_extend_batch(pirrt_ctx* c, int32_t n_new, const double* points, uint32_t flags,
+                       int32_t* n_new_promising, int64_t* n_edges_out) {
+    if (!c) return fail(PIRRT_E_INVAL, "extend: NULL context");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
+    if (c->w_d == 0) return fail(PIRRT_E_STATE, "extend: no world (pirrt_set_world)");
+    if (n_new < 0 || (n_new > 0 && !points)) return fail(PIRRT_E_INVAL, "extend: bad arguments");
+    if ((int64_t)c->n + n_new > INT32_MAX - 1) return fail(PIRRT_E_RANGE, "extend: too many vertices");
+    const int d = c->w_d, n_old = c->n, n_all = c->n + n_new;
+    const bool dev = (flags & PIRRT_F_DEVICE_PTRS) != 0;
+    cudaStream_t s = c->stream;
+    if (n_new == 0) {
+        if (n_edges_out) *n_edges_out = 0;
+        return pirrt_graph_append_batch(c, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr,
+                                        0, n_new_promising);
+    }
+    // points of the new vertices go to slots >= n (invisible until the append commits)
+    if ((rc = grow(c->pts, c->pts_cap, (int64_t)n_all * d, (int64_t)n_old * d, s))) return rc;
+    CU(cudaMemcpyAsync(c->pts + (int64_t)n_old * d, points, sizeof(double) * n_new * d,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    // connection radii r(i + 1) = gamma (ln m / m)^(1/d), m = i + 1 (host libm,
+    // the same as the CPU generator's), and the grid: cells of side >= the
+    // largest radius of the batch (that of its first vertex), so a neighbour
+    // lies in the 3^d cells around a point; at most 4 n_all cells
+    std::vector<double> R(n_new);
+    for (int t = 0; t < n_new; ++t) {
+        const double m = (double)(n_old + t) + 1.0;
+        R[t] = m < 2.0 ? 1e300 : c->w_gamma * std::pow(std::log(m) / m, 1.0 / d);
+    }
+    int mc = R[0] >= 1.0 ? 1 : (int)std::floor(1.0 / (R[0] * (1.0 + 1e-9)));
+    while (mc > 1 && std::pow((double)mc, d) > 4.0 * (double)n_all) --mc;
+    const int brute = mc < 3 ? 1 : 0;
+    long long ncell = 1;
+    if (!brute) for (int k = 0; k < d; ++k) ncell *= mc;
+    if ((rc = grow(c->x_R, c->x_R_cap, n_new, 0, s))) return rc;
+    if ((rc = grow(c->x_h, c->x_h_cap, n_new, 0, s))) return rc;
+    if ((rc = grow(c->x_ecnt, c->x_ecnt_cap, n_new + 1, 0, s))) return rc;
+    if ((rc = grow(c->x_eoff, c->x_eoff_cap, n_new + 1, 0, s))) return rc;
+    if ((rc = grow(c->x_tmp, c->x_tmp_cap, (int64_t)std::max(scan_tmp_elems(ncell + 1), scan_tmp_elems(n_new + 1)), 0, s))) return rc;
+    if (!brute) {
+        if ((rc = grow(c->x_cell, c->x_cell_cap, n_all, 0, s))) return rc;
+        if ((rc = grow(c->x_cpts, c->x_cpts_cap, n_all, 0, s))) return rc;
+        if ((rc = grow(c->x_ccnt, c->x_ccnt_cap, ncell + 1, 0, s))) return rc;
+        if ((rc = grow(c->x_cstart, c->x_cstart_cap, ncell + 1, 0, s))) return rc;
+    }
+    CU(cudaMemcpyAsync(c->x_R, R.data(), sizeof(double) * n_new, cudaMemcpyHostToDevice, s));
+    ExtendArgs a;
+    a.pts = c->pts; a.n_old = n_old; a.n_new = n_new; a.d = d; a.m = mc; a.brute = brute;
+    a.ncell = ncell; a.cell = c->x_cell; a.ccnt = c->x_ccnt; a.cstart = c->x_cstart; a.cpts = c->x_cpts;
+    a.scan_tmp = c->x_tmp; a.R = c->x_R; a.boxes = c->w_boxes; a.n_boxes = c->w_nboxes;
+    a.x_goal = c->w_goal; a.h_new = c->x_h; a.ecnt = c->x_ecnt; a.eoff = c->x_eoff;
+    a.src = nullptr; a.dst = nullptr; a.cost = nullptr;
+    const long long l0 = g_kernel_launches;
+    CU(launch_extend_grid(a, s));
+    long long total = 0;
+    CU(cudaMemcpyAsync(&total, c->x_eoff + n_new, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if ((rc = grow(c->x_src, c->x_src_cap, std::max<long long>(1, total), 0, s))) return rc;
+    if ((rc = grow(c->x_dst, c->x_dst_cap, std::max<long long>(1, total), 0, s))) return rc;
+    if ((rc = grow(c->x_cost, c->x_cost_cap, std::max<long long>(1, total), 0, s))) return rc;
+    a.src = c->x_src; a.dst = c->x_dst; a.cost = c->x_cost;
+    if (total > 0) CU(launch_extend_edges(a, s));
+    c->launches += g_kernel_launches - l0;
+    if (n_edges_out) *n_edges_out = total;
+    // the ordinary append (a1): store, Extend's local relaxation, promising test
+    c->in_extend = true;
+    rc = pirrt_graph_append_batch(c, n_new, c->x_h, nullptr, nullptr, total, c->x_src, c->x_dst,
+                                  c->x_cost,
+                                  PIRRT_F_EDGES_UNDIRECTED | PIRRT_F_DEVICE_PTRS | (flags & PIRRT_F_VALIDATE),
+                                  n_new_promising);
+    c->in_extend = false;
+    return rc;
+}
+
+int pirrt_get_points(const pirrt_ctx* c, double* out, int64_t cap) {
+    if (!c || !out) return fail(PIRRT_E_INVAL, "get_points: NULL argument");
+    if (c->w_d == 0) return fail(PIRRT_E_STATE, "get_points: no world");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if (cap < (int64_t)c->n * c->w_d) return fail(PIRRT_E_RANGE, "get_points: capacity too small");
+    CU(cudaMemcpyAsync(out, c->pts, sizeof(double) * c->n * c->w_d, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     return PIRRT_OK;
 }
 

@@ -271,6 +271,29 @@ cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* 
                                  long long* cnt, long long* scan_tmp, cudaStream_t s);
 
 // best goal (lowest g, lowest id on ties) and its branch; see k_best_path
+// device-side Extend (extend.cu)
+struct ExtendArgs {
+    const double* pts;            // all points [n_old + n_new][d] (new ones staged)
+    int n_old, n_new, d;
+    int m, brute;                 // grid cells per axis (cell side >= every radius); brute: no grid
+    long long ncell;
+    int* cell;                    // [n_all] cell id per point
+    long long* ccnt;              // [ncell + 1] counts / cursors
+    long long* cstart;            // [ncell + 1] exclusive scan
+    int* cpts;                    // [n_all] point ids by cell
+    long long* scan_tmp;
+    const double* R;              // [n_new] r(i + 1), computed on the host
+    const double* boxes;          // [n_boxes][2][d]
+    int n_boxes;
+    const double* x_goal;         // [d]
+    double* h_new;                // [n_new] out
+    long long* ecnt;              // [n_new + 1] edges per new vertex
+    long long* eoff;              // [n_new + 1] their offsets (eoff[n_new] = total)
+    int* src; int* dst; double* cost;   // [total] COO out (undirected: j -> i stored once)
+};
+cudaError_t launch_extend_grid(const ExtendArgs& a, cudaStream_t s);   // grid, h, counts, offsets
+cudaError_t launch_extend_edges(const ExtendArgs& a, cudaStream_t s);  // the triples
+
 cudaError_t launch_best_path(const int* parent, const double* g, int n, const int* goals,
                              int n_goals, int* out, cudaStream_t s);
 

@@ -45,6 +45,7 @@ EXPORTS = (
     "pirrt_exploit", "pirrt_exploit_async", "pirrt_exploit_wait", "pirrt_get_policy",
     "pirrt_get_costs", "pirrt_get_promising", "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
     "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id",
+    "pirrt_set_world", "pirrt_extend_batch", "pirrt_get_points",
     # include/pirrt_bench.h (measurement helpers)
     "pirrt_bench_rows", "pirrt_bench_relax", "pirrt_bench_gather",
 )
@@ -104,6 +105,9 @@ def _load():
                                              C.c_uint32, P]
     lib.pirrt_exploit.argtypes = [P, C.POINTER(pirrt_exploit_stats)]
     lib.pirrt_exploit_async.argtypes = [P]
+    lib.pirrt_set_world.argtypes = [P, C.c_int32, C.c_int32, P, P, P, C.c_double]
+    lib.pirrt_extend_batch.argtypes = [P, C.c_int32, P, C.c_uint32, P, P]
+    lib.pirrt_get_points.argtypes = [P, P, C.c_int64]
     lib.pirrt_exploit_wait.argtypes = [P, C.POINTER(pirrt_exploit_stats)]
     for f in ("pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
               "pirrt_get_parent_costs"):
@@ -133,6 +137,9 @@ pirrt_destroy = _lib.pirrt_destroy
 pirrt_graph_append_batch = _lib.pirrt_graph_append_batch
 pirrt_exploit = _lib.pirrt_exploit
 pirrt_exploit_async = _lib.pirrt_exploit_async
+pirrt_set_world = _lib.pirrt_set_world
+pirrt_extend_batch = _lib.pirrt_extend_batch
+pirrt_get_points = _lib.pirrt_get_points
 pirrt_exploit_wait = _lib.pirrt_exploit_wait
 pirrt_get_policy = _lib.pirrt_get_policy
 pirrt_get_costs = _lib.pirrt_get_costs
@@ -293,6 +300,33 @@ class Context:
         st = pirrt_exploit_stats()
         _check(pirrt_exploit(self._h, C.byref(st)))
         return ExploitStats(*(getattr(st, f[0]) for f in pirrt_exploit_stats._fields_))
+
+    def set_world(self, d, boxes, x_init, x_goal, gamma):
+        """pirrt_set_world: [0,1]^d, boxes (n_boxes, 2, d), x_init, x_goal, gamma."""
+        boxes = np.ascontiguousarray(boxes, np.float64).reshape(-1)
+        xi = np.ascontiguousarray(x_init, np.float64)
+        xg = np.ascontiguousarray(x_goal, np.float64)
+        nb = boxes.size // (2 * int(d))
+        _check(pirrt_set_world(self._h, int(d), nb, boxes.ctypes.data if nb else None,
+                               xi.ctypes.data, xg.ctypes.data, float(gamma)))
+        self.d = int(d)
+
+    def extend(self, points, flags=0):
+        """pirrt_extend_batch: (n_new_promising, undirected pairs created)."""
+        nprom, ne = C.c_int32(0), C.c_int64(0)
+        if _is_torch_cuda(points):
+            flags |= PIRRT_F_DEVICE_PTRS
+            n, ptr = int(points.shape[0]), points.data_ptr()
+        else:
+            points = np.ascontiguousarray(points, np.float64)
+            n, ptr = int(points.shape[0]), (points.ctypes.data if points.size else None)
+        _check(pirrt_extend_batch(self._h, n, ptr, int(flags), C.byref(nprom), C.byref(ne)))
+        return int(nprom.value), int(ne.value)
+
+    def points(self):
+        out = np.empty((self.n, self.d), np.float64)
+        _check(pirrt_get_points(self._h, out.ctypes.data, out.size))
+        return out
 
     def exploit_async(self) -> None:
         """pirrt_exploit_async: start the exploit and return at once."""

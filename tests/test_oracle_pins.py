@@ -474,3 +474,12 @@ def test_B_members_beat_goal_cost(seed):
         assert np.all(g[idx] + r.h[idx] < thr)
         checked += idx.size
     assert checked > 0
+
+
+def test_gen_points_equal_rrg_samples():
+    # the sampling-only generator (for the device-side Extend) reproduces the
+    # full generator's boxes and points bit for bit
+    for d, nb in ((2, 0), (3, 5), (6, 20)):
+        r = gen.rrg(d, 3000, gen.gamma_k(d), n_boxes=nb, seed=gen.seed_of("pts", d))
+        p, b = gen.points(d, 3000, nb, seed=gen.seed_of("pts", d))
+        assert np.array_equal(p, r.points) and np.array_equal(b, r.boxes)
