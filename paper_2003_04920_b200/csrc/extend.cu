@@ -92,6 +92,11 @@ __device__ __forceinline__ bool seg_hits_box(const double* q, const double* p, c
 // one warp per new vertex i = n_old + t: every earlier j in the 3^d cells
 // around x_i (or all j < i when brute) with |x_i - x_j| <= R_t and a free
 // segment.  WRITE = false: count into cnt[t]; true: write at off[t].
+// The stencil is taken 32 cells at a time (one per lane): a lane drops a
+// cell the R-ball misses and loads the range of a kept one; the candidates
+// of the kept cells, concatenated by a warp scan of their counts, are then
+// tested 32 at a time (owner cell of a candidate by a binary search over the
+// lanes' prefix), so every lane works whatever the cell occupancy.
 template <bool WRITE>
 __global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_new, int d, int m,
                              int brute, const long long* __restrict__ cstart,
@@ -101,56 +106,87 @@ __global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_ne
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int t = w; t < n_new; t += nw) {
+    unsigned lt;
+    asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
+    for (int t = w; t < n_new; t += nw) {                 // warp-uniform
         const int i = n_old + t;
         const double* p = pts + (long long)i * d;
         const double Ri = R[t];
+        const double R2cut = Ri * Ri * (1.0 + 1e-9);      // conservative: never prunes a neighbour
+        const double inv_m = 1.0 / m;
         long long found = 0;
-        long long base = WRITE ? off[t] : 0;
-        int cc[16], lo[16], hi[16];
-        int ncells = 1;
+        const long long base = WRITE ? off[t] : 0;
+        int lo[16], rad[16];
+        int N = 1;
         if (!brute) {
             for (int k = 0; k < d; ++k) {
                 const int c = cell_coord(p[k], m);
                 lo[k] = c > 0 ? c - 1 : 0;
-                hi[k] = c < m - 1 ? c + 1 : m - 1;
-                cc[k] = lo[k];
-                ncells *= hi[k] - lo[k] + 1;
+                rad[k] = (c < m - 1 ? c + 1 : m - 1) - lo[k] + 1;
+                N *= rad[k];
             }
         }
-        const double inv_m = 1.0 / m;
-        const double R2cut = Ri * Ri * (1.0 + 1e-9);      // conservative: never prunes a neighbour
-        for (int ci = 0; ci < ncells; ++ci) {
-            long long a0, a1;
-            if (brute) { a0 = 0; a1 = i; }
-            else {
+        for (int s0 = 0; s0 < N; s0 += 32) {
+            // this lane's stencil cell
+            long long a0 = 0;
+            int len = 0;
+            const int sidx = s0 + lane;
+            if (brute) {
+                if (lane == 0) len = i;                   // all j < i, in id order
+            } else if (sidx < N) {
+                int r = sidx;
                 long long c = 0;
                 double gap2 = 0.0;                        // squared distance from x_i to the closed cell
-                for (int k = 0; k < d; ++k) {
-                    c = c * m + cc[k];
-                    const double clo = cc[k] * inv_m, chi = (cc[k] + 1) * inv_m;
+                for (int k = d - 1; k >= 0; --k) {        // mixed-radix digits, last axis fastest
+                    const int cc = lo[k] + r % rad[k];
+                    r /= rad[k];
+                    const double clo = cc * inv_m, chi = (cc + 1) * inv_m;
                     const double g = p[k] < clo ? clo - p[k] : (p[k] > chi ? p[k] - chi : 0.0);
                     gap2 += g * g;
+                    (void)cc;
                 }
-                for (int k = d - 1; k >= 0; --k) {      // next cell (odometer)
-                    if (cc[k] < hi[k]) { ++cc[k]; break; }
-                    cc[k] = lo[k];
+                if (gap2 <= R2cut) {
+                    r = sidx;
+                    long long mult = 1;
+                    for (int k = d - 1; k >= 0; --k) {
+                        c += (long long)(lo[k] + r % rad[k]) * mult;
+                        r /= rad[k];
+                        mult *= m;
+                    }
+                    a0 = cstart[c];
+                    len = (int)(cstart[c + 1] - a0);
                 }
-                if (gap2 > R2cut) continue;               // the R-ball misses this cell
-                a0 = cstart[c]; a1 = cstart[c + 1];
             }
-            for (long long e0 = a0; e0 < a1; e0 += 32) {   // warp-uniform
-                const long long e = e0 + lane;
+            int incl = len;                               // warp scan of the candidate counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - len;
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            for (int k0 = 0; k0 < total; k0 += 32) {       // warp-uniform
+                const int k = k0 + lane;
+                int own = 0;                              // last lane whose prefix <= k
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int cand = own + step;
+                    const int ex = __shfl_sync(0xffffffffu, excl, cand);
+                    if (ex <= k) own = cand;
+                }
+                const long long ba = __shfl_sync(0xffffffffu, a0, own);
+                const int be = __shfl_sync(0xffffffffu, excl, own);
                 bool hit = false;
                 int j = -1;
                 double dd = 0.0;
-                if (e < a1) {
+                if (k < total) {
+                    const long long e = ba + (k - be);
                     j = brute ? (int)e : cpts[e];
                     if (j < i) {
                         const double* q = pts + (long long)j * d;
                         double s2 = 0.0;
-                        for (int k = 0; k < d; ++k) {
-                            const double u = p[k] - q[k];
+                        for (int kk = 0; kk < d; ++kk) {
+                            const double u = p[kk] - q[kk];
                             s2 += u * u;
                         }
                         dd = sqrt(s2);
@@ -163,13 +199,12 @@ __global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_ne
                 }
                 const unsigned mask = __ballot_sync(0xffffffffu, hit);
                 if (WRITE && hit) {
-                    unsigned lt;
-                    asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
                     const long long o = base + found + __popc(mask & lt);
                     src[o] = j; dst[o] = i; cost[o] = dd;
                 }
                 found += __popc(mask);
             }
+            if (brute) break;
         }
         if (!WRITE && lane == 0) cnt[t] = found;
     }
