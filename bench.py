@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graph-cache", default="", help="npz path to reuse a generated graph")
+    ap.add_argument("--grid-blocks", type=int, default=0,
+                    help="persistent exploit grid (0 = SMs x occupancy)")
     ap.add_argument("--sharded", action="store_true",
                     help="one graph split over the ranks (NCCL sharded exploit, strong scaling) "
                          "instead of independent replicas (weak scaling)")
@@ -201,7 +203,8 @@ def run_cuda(a, rank, world):
         shard_kw = dict(nranks=world, rank=rank, nccl_id=nid,
                         flags=pirrt.PIRRT_F_SHARDED if world == 1 else 0)
     ctx = pirrt.Context(h_root=g.h_root(), stream=stream, vertex_capacity=g.n + 1024,
-                        edge_capacity=int(2.4 * g.off[-1]) + 4096, **shard_kw)
+                        edge_capacity=int(2.4 * g.off[-1]) + 4096, grid_blocks=a.grid_blocks,
+                        **shard_kw)
     # ---- pre-load: BE-RRT# history up to dev0 (untimed)
     t0 = time.perf_counter()
     replay(ctx, g, a.S, n_stop=dev0, final=False)

@@ -13,8 +13,9 @@
 //
 // Kernels: a uniform grid of cell side >= the batch's largest radius over all
 // points so far (cell id, histogram, scan, scatter), then one warp per new
-// vertex scanning its 3^d neighbour cells twice -- count, then write the COO
-// triples (src = j, dst = i, cost) at scanned offsets.  The triples feed the
+// vertex over its 3^d neighbour cells (cells the R-ball misses dropped),
+// twice -- count, then write the COO triples (src = j, dst = i, cost) at
+// scanned offsets.  The triples feed the
 // ordinary append (a1) with device pointers; nothing is committed here.
 #include <cuda_runtime.h>
 
@@ -143,7 +144,6 @@ __global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_ne
                     const double clo = cc * inv_m, chi = (cc + 1) * inv_m;
                     const double g = p[k] < clo ? clo - p[k] : (p[k] > chi ? p[k] - chi : 0.0);
                     gap2 += g * g;
-                    (void)cc;
                 }
                 if (gap2 <= R2cut) {
                     r = sidx;
