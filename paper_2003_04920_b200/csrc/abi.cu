@@ -713,6 +713,12 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     return PIRRT_OK;
 }
 
+// the exploit-kernel instantiation with the children-index Evaluate is used
+// when a large Evaluate is possible: PRUNE_OFF, or |B| already >= kids_min
+static int kids_variant(const ExploitArgs& a, int Bcount) {
+    return a.kids_min > 0 && (a.prune_off || (int64_t)Bcount + a.n_goals >= a.kids_min) ? 1 : 0;
+}
+
 static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     std::memset(&a, 0, sizeof(a));
     a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
@@ -750,6 +756,7 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.coff = (int*)c->cnt;
     a.kids = (int*)c->cnt + (c->vcap + 1);
     a.kids_bsum = (int*)c->app_bsum;
+    a.kids_variant = kids_variant(a, c->Bcount);
 }
 
 // Sharded exploit: per PI iteration
@@ -804,6 +811,7 @@ static int exploit_sharded(pirrt_ctx* c) {
         NC(api->allGather(c->rec_local, c->rec_all, (size_t)stride * sizeof(ShardRec), ncclChar,
                           c->comm, s));
         a.pending = 0;   // leave_B was done by the Improve kernel
+        a.kids_variant = kids_variant(a, Bc);
         CU(launch_shard_evaluate(a, it, c->rec_all, c->rec_counts + 1, stride, c->nranks,
                                  c->shard_blocks, s));
         c->launches += 1;
@@ -873,6 +881,7 @@ int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
             w.Bsel = h.Bsel_out; w.Bcount = h.Bcount_out; w.old_Bcount = h.old_Bcount_out;
             w.pending = h.pending_out;
             w.ev_base = c->ev_next + (unsigned)h.evaluations;
+            w.kids_variant = w.kids_variant || kids_variant(w, w.Bcount);
             const int it = h.handoff_it;
             CU(cudaMemsetAsync(&c->ctl->handoff, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), s));
             cudaError_t e;

@@ -146,6 +146,7 @@ struct ExploitArgs {
     int* coff;                        // [n]: after the build row(p) = [p ? coff[p-1] : 0, coff[p])
     int* kids;                        // [n]
     int* kids_bsum;                   // [grid blocks] scan partials
+    int kids_variant;                 // launch the instantiation that can use the index
 };
 
 // ---- goal set (reading R4, goal-set form) ----

@@ -393,3 +393,16 @@ def test_sharded_loop_wide_improve(P, monkeypatch):
         gpu = P.Context(h_root=r.h_root(), flags=flags | P.PIRRT_F_SHARDED)
         orc = Oracle(h_root=r.h_root(), flags=flags)
         dual_replay(gpu, orc, r, 2000)
+
+
+@pytest.mark.parametrize("gb", [1, 2])
+@pytest.mark.parametrize("flags", [0, PRUNE_OFF])
+def test_children_index_wide_levels_few_blocks(P, monkeypatch, gb, flags):
+    # few blocks: every block's share of a level exceeds its thread count
+    # (one item per thread over the children index) and its push staging
+    # overflows into the queue (warp-aggregated reservations)
+    monkeypatch.setenv("PIRRT_KIDS_MIN", "1")
+    r = gen.rrg(6, 15000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("kids-wide", gb, flags))
+    gpu = P.Context(h_root=r.h_root(), flags=flags, grid_blocks=gb)
+    orc = Oracle(h_root=r.h_root(), flags=flags)
+    dual_replay(gpu, orc, r, r.n // 2)
