@@ -28,11 +28,17 @@ def main():
     ap.add_argument("--S", type=int, default=65536)
     ap.add_argument("--batches", type=int, default=10)
     ap.add_argument("--out", default="gpurun_out/cfg5.json")
+    ap.add_argument("--d", type=int, default=6)
+    ap.add_argument("--gamma", default="k")
+    ap.add_argument("--boxes", type=int, default=20)
+    ap.add_argument("--seed-tag", default="", help="gen.seed_of tag (default: cfg5_extend)")
     a = ap.parse_args()
-    d, gamma, boxes = 6, gen.gamma_k(6), 20
+    d, boxes = a.d, a.boxes
+    gamma = gen.gamma_k(d) if a.gamma == "k" else gen.gamma_star(d)
     n_all = a.n + a.batches * a.S
     t0 = time.perf_counter()
-    pts, bx = gen.points(d, n_all, boxes, seed=gen.seed_of("cfg5_extend", a.n))
+    seed = gen.seed_of(a.seed_tag) if a.seed_tag else gen.seed_of("cfg5_extend", a.n)
+    pts, bx = gen.points(d, n_all, boxes, seed=seed)
     t_pts = time.perf_counter() - t0
     h_root = float(np.sqrt(((pts[0] - pts[1]) ** 2).sum()))
     # warm-up (first-call costs)
@@ -43,7 +49,8 @@ def main():
             w.exploit()
     del w
     ctx = pirrt.Context(h_root=h_root, stream=torch.cuda.current_stream(),
-                        vertex_capacity=n_all + 1024, edge_capacity=int(2.2 * 40 * n_all))
+                        vertex_capacity=n_all + 1024,
+                        edge_capacity=int(2.2 * (40 if a.gamma == "k" else 600) * n_all))
     ctx.set_world(d, bx, pts[0], pts[1], gamma)
     dpts = torch.from_numpy(pts).cuda()
     torch.cuda.synchronize()
