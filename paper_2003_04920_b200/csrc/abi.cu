@@ -201,6 +201,7 @@ struct pirrt_ctx {
     int wq_wide = -1;                                        // PIRRT_WQ_WIDE (-1: 10 per block, 0: off)
     int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
     int wide_tasks = 131072;                                 // PIRRT_WIDE_TASKS: |I| for the wide Improve (0: off)
+    int fuse_root = 1;                                       // PIRRT_FUSE_ROOT=0: root level with its own barrier
     int kids_min = -1;                                       // PIRRT_KIDS_MIN: |B| for the children index
                                                              // (-1: 4 n / mean degree; 0: never)
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
@@ -491,6 +492,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
     if (const char* w = std::getenv("PIRRT_WIDE_TASKS")) c->wide_tasks = std::max(0, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_KIDS_MIN")) c->kids_min = std::atoi(w);
+    if (const char* w = std::getenv("PIRRT_FUSE_ROOT")) c->fuse_root = std::atoi(w);
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -742,6 +744,7 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.wq_tail = c->wq_tail < 0 ? 16 * c->grid_blocks : std::min(c->wq_tail, 64 * c->grid_blocks);
     a.wq_wide = c->wq_wide < 0 ? 10 * c->grid_blocks : c->wq_wide;
     a.halves = c->halves;
+    a.fuse_root = c->fuse_root;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
     a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;
     a.goals = c->goals; a.n_goals = (int)c->goals_host.size();

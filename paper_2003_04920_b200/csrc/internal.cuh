@@ -44,6 +44,7 @@ struct IterCtl {
     int qtail;                    // slots reserved by publishers
     int qout;                     // (children created - items expanded): -F0 = done
     int bcnt;                     // entries written to the new B list
+    int l1cnt;                    // fused root levels: expanded children of the root
 };
 
 // One Improve result in sharded mode (all-gathered between ranks).
@@ -147,6 +148,7 @@ struct ExploitArgs {
     int* kids;                        // [n]
     int* kids_bsum;                   // [grid blocks] scan partials
     int kids_variant;                 // launch the instantiation that can use the index
+    int fuse_root;                    // Evaluate levels 0 and 1 without a grid barrier between
 };
 
 // ---- goal set (reading R4, goal-set form) ----

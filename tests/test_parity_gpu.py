@@ -406,3 +406,16 @@ def test_children_index_wide_levels_few_blocks(P, monkeypatch, gb, flags):
     gpu = P.Context(h_root=r.h_root(), flags=flags, grid_blocks=gb)
     orc = Oracle(h_root=r.h_root(), flags=flags)
     dual_replay(gpu, orc, r, r.n // 2)
+
+
+@pytest.mark.parametrize("fuse", ["0", "1"])
+@pytest.mark.parametrize("gb", [1, 3, 0])
+def test_fused_root_levels_parity(P, monkeypatch, fuse, gb):
+    # Evaluate levels 0 and 1 without a barrier (every block owns the root's
+    # children at its row positions) or with one; with 1 or 3 blocks the
+    # root's row may exceed the owned capacity (fallback to the plain level)
+    monkeypatch.setenv("PIRRT_FUSE_ROOT", fuse)
+    r = gen.rrg(6, 12000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("fuse-root", gb))
+    gpu = P.Context(h_root=r.h_root(), grid_blocks=gb)
+    orc = Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, 700)
