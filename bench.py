@@ -328,6 +328,7 @@ def run_cuda(a, rank, world):
         "e2e_sync_steps": len(e2e_ms), "h2d": h2d / a.steps, "d2h": d2h / a.steps,
         "clocks": clk, "t_gen": t_gen, "t_pre": t_pre,
         "iters": [s.iterations for s in ex], "prom": [s.promising for s in ex],
+        "exploit_ms_list": [s.device_ms for s in ex],
         "improve_ms": sum(s.improve_ms for s in ex), "evaluate_ms": sum(s.evaluate_ms for s in ex),
         "barriers": sum(s.barriers for s in ex),
         "improve_bytes": sum(s.relaxations * B_RELAX + s.improve_set * B_IVERT for s in ex),
@@ -380,6 +381,17 @@ def cpu_info():
     except OSError:
         pass
     return model, os.cpu_count()
+
+
+def step_stats(xs):
+    xs = sorted(float(x) for x in xs)
+    if not xs:
+        return None
+    m = statistics.mean(xs)
+    return {"median": round(statistics.median(xs), 4),
+            "p95": round(xs[min(len(xs) - 1, int(round(0.95 * (len(xs) - 1))))], 4),
+            "mean": round(m, 4), "std": round(statistics.pstdev(xs), 4),
+            "min": round(xs[0], 4), "max": round(xs[-1], 4)}
 
 
 def peaks():
@@ -438,6 +450,9 @@ def main():
         "steps": a.steps,
         "warmup": a.warmup,
         "ms_per_step": round(ms_step, 4),
+        # per-step distribution on this rank (P:498-499 report trials)
+        "step_ms_stats": step_stats(res["step_ms"]),
+        "exploit_ms_stats": step_stats(res["exploit_ms_list"]),
         "higher_is_better": False,
         "scaling": "strong" if a.sharded else "weak",
         "vs_baseline": None,
