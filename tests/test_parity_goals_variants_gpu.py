@@ -234,3 +234,45 @@ def test_async_exploit_wait_without_start(P):
     gpu.exploit_wait()
     with pytest.raises(P.PirrtError):
         gpu.exploit_wait()
+
+
+# ------------------------------------------------------------ combinations
+
+@pytest.mark.parametrize("env", [{"PIRRT_KIDS_MIN": "1"}, {"PIRRT_KIDS_MIN": "1", "PIRRT_FUSE_ROOT": "0"},
+                                 {"PIRRT_WIDE_TASKS": "1"}])
+def test_parent_form_goal_set_with_index_and_wide_improve(P, monkeypatch, env):
+    # the KIDS and parent-form instantiations together, and every Improve
+    # through the full-occupancy launch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    r = gen.rrg(6, 10000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("combo", len(env)))
+    ids, h = goal_region(r, 0.3)
+    gpu, orc = pair(P, h_root=h[0], parent_form=True, goals=ids)
+    dual_replay(gpu, orc, with_h(r, h), 1200)
+
+
+def test_extend_with_goal_set_parent_form_and_async(P):
+    # device-side Extend + goal set + parent form + the asynchronous exploit
+    from oracle import EDGES_UNDIRECTED
+    from paper_2003_04920_b200.berrt import batches
+    r = gen.rrg(4, 8000, gen.gamma_k(4), n_boxes=12, seed=gen.seed_of("combo-extend"))
+    ids, _ = goal_region(r, 0.15)
+    # the device computes h = |x - x_goal| itself, as the generator does (r.h)
+    gpu, orc = pair(P, h_root=r.h_root(), parent_form=True, goals=ids)
+    gpu.set_world(4, r.boxes, r.points[0], r.points[1], gen.gamma_k(4))
+    started = False
+    for k, (a, b) in enumerate(batches(r.n, 300)):
+        pg, ne = gpu.extend(r.points[a:b])
+        if started:
+            assert_same_stats(gpu.exploit_wait(), ost, f"batch {k}")
+            started = False
+        s, d_, c = r.batch(a, b, directed=False)
+        po = orc.append(r.h[a:b], s, d_, c, flags=EDGES_UNDIRECTED)
+        assert pg == po and ne == s.size
+        if po > 0:
+            ost = orc.exploit()
+            gpu.exploit_async()
+            started = True
+    if started:
+        assert_same_stats(gpu.exploit_wait(), ost, "last")
+    assert_same_state(gpu, orc, "final")
