@@ -381,7 +381,10 @@ int stage(pirrt_ctx* c, const T* src, int64_t count, bool device, T*& buf, int64
 }
 
 int read_ctl(pirrt_ctx* c) {
-    CU(cudaMemcpyAsync(c->ctl_host, c->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, c->stream));
+    // everything after the per-iteration counters (the host never reads those)
+    const size_t o = offsetof(DevCtl, status);
+    CU(cudaMemcpyAsync((char*)c->ctl_host + o, (const char*)c->ctl + o, sizeof(DevCtl) - o,
+                       cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return 0;
 }

@@ -29,22 +29,29 @@ enum : int {
 // Per-iteration counters of the exploit loop, double-buffered by iteration
 // parity so that one phase can reset the other copy without a race.
 struct IterCtl {
-    unsigned long long dg_bits;   // atomicMax of Delta g (non-negative f64 bits)
-    long long relax;              // relaxations this Improve
-    long long visits;             // children visited this Evaluate
-    long long scanned;            // out-row entries scanned this Evaluate
-    int tasks;                    // |I|
-    int ptr_changed;              // some parent value changed in Improve
-    int g_changed;                // some g bit changed in Evaluate
-    int both;                     // |old B  n  new B|
-    int lpush[3];                 // expanded vertices per BFS level (rotating slots)
-    int lvis[3];                  // "some child visited" per BFS level (rotating slots)
-    // work-queue Evaluate: queue slot 0 holds the root permanently
-    int qhead;                    // slots claimed by blocks
-    int qtail;                    // slots reserved by publishers
-    int qout;                     // (children created - items expanded): -F0 = done
-    int bcnt;                     // entries written to the new B list
-    int l1cnt;                    // fused root levels: expanded children of the root
+    // Every counter that all blocks update (one atomic per block per phase or
+    // level) or poll has its own 128-byte line: on a shared line ~300 blocks'
+    // atomics and polls serialise at one L2 slice (4-5% of the bench step).
+    alignas(128) unsigned long long dg_bits;   // atomicMax of Delta g (non-negative f64 bits)
+    alignas(128) long long relax;              // relaxations this Improve
+    alignas(128) int tasks;                    // |I|
+    alignas(128) int ptr_changed;              // some parent value changed in Improve
+    alignas(128) long long visits;             // children visited this Evaluate
+    long long scanned;                         // out-row entries scanned this Evaluate
+    int g_changed;                             // some g bit changed in Evaluate
+    int both;                                  // |old B  n  new B|
+    struct alignas(128) Level {                // rotating per-level slots
+        int push;                              // expanded vertices of the level
+        int vis;                               // "some child visited" at the level
+    } lv[3];
+    // work-queue Evaluate: queue slot 0 holds the root permanently; waiting
+    // blocks poll qhead / qtail / qout while working blocks update qtail,
+    // qout and bcnt
+    alignas(128) int qhead;                    // slots claimed by blocks
+    alignas(128) int qtail;                    // slots reserved by publishers
+    alignas(128) int qout;                     // (children created - items expanded): -F0 = done
+    alignas(128) int bcnt;                     // entries written to the new B list
+    alignas(128) int l1cnt;                    // fused root levels: expanded children of the root
 };
 
 // One Improve result in sharded mode (all-gathered between ranks).
