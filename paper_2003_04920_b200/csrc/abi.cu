@@ -663,7 +663,8 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     if ((rc = grow(c->odidx[nb], c->odidx_cap[nb], dneed, 0, s))) return rc;
     if (early) CU(cudaStreamWaitEvent(s, c->copy_done, 0));
     else if ((rc = stage_all(s))) return rc;
-    CU(cudaMemsetAsync(&c->ctl->err, 0, 4 * sizeof(int), s));   // err, nprom, sweeps
+    CU(cudaMemsetAsync(&c->ctl->err, 0, 2 * sizeof(int), s));   // err, sweeps
+    CU(cudaMemsetAsync(&c->ctl->nprom, 0, sizeof(int), s));
     CU(cudaMemsetAsync(&c->ctl->sweep_changed[0], 0, 2 * sizeof(int), s));
     AppendArgs a;
     a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;

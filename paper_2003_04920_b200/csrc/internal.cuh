@@ -85,12 +85,11 @@ struct DevCtl {
     // improve_wide_kernel for it and resumes the loop after that Improve
     int handoff, handoff_it;
     unsigned long long t_wide0, t_wide1;   // ~min start / max end of the wide Improve
-    // append / set_policy
-    int err;                      // bitmask of kErr*
-    int nprom;                    // new promising vertices
+    // append / set_policy (the words every block may update on their own lines)
+    alignas(128) int err;         // bitmask of kErr*
     int sweeps;                   // local-relaxation sweeps
-    int sweep_changed[2];
-    int pad2;
+    alignas(128) int nprom;       // new promising vertices
+    alignas(128) int sweep_changed[2];
 };
 
 // Everything the persistent exploit kernel touches.

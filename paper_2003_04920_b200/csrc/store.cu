@@ -753,7 +753,9 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
                     }
                 }
             }
-            if (my_change) atomicOr(chg, 1);
+            // one flag update per block, and none once some block has set it
+            if (__syncthreads_or(my_change) && threadIdx.x == 0 && *(volatile int*)chg == 0)
+                atomicOr(chg, 1);
             grid.sync();
             const int any = *(volatile int*)chg;
             if (lead) ctl->sweeps = sw + 1;
