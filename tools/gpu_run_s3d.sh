@@ -1,0 +1,6 @@
+timeout 1200 python -m pytest tests/test_parity_gpu.py tests/test_parity_goals_variants_gpu.py -m gpu -x -q 2>&1 | tail -2
+for i in 1 2 3; do
+for lib in libpirrt_prev.so libpirrt.so; do
+  PIRRT_LIB=paper_2003_04920_b200/lib/$lib python bench.py --no-cpu-baseline --graph-cache /tmp/g_bench8.npz 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('$lib', d['value'], d['exploit_ms_mean'], d['append_plus_readout_ms_mean'], d['phase_ms'])"
+done
+done
