@@ -121,6 +121,7 @@ struct pirrt_ctx {
     bool own_stream = false;
     int num_sms = 0;
     int grid_blocks = 0;
+    int append_per_sm = 0;        // k_append_fused occupancy (computed at create)
     int n = 0;
     int64_t vcap = 0;
     // vertex SoA
@@ -515,6 +516,8 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (!prop.cooperativeLaunch) return bail(fail(PIRRT_E_STATE, "create: no cooperative launch"));
     int per_sm = exploit_blocks_per_sm();
     if (per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: exploit kernel does not fit an SM"));
+    c->append_per_sm = append_blocks_per_sm();
+    if (c->append_per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: append kernel does not fit an SM"));
     c->grid_blocks = cfg.grid_blocks > 0 ? std::min(cfg.grid_blocks, per_sm * c->num_sms)
                                          : per_sm * c->num_sms;
     c->grid_blocks = std::min(c->grid_blocks, kMaxGridBlocks);
@@ -686,6 +689,7 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     a.n_old = n_old; a.n_new = n_new; a.base_edges = c->base_edges;
     a.ctl = c->ctl;
     a.grid_blocks = c->num_sms;
+    a.per_sm = c->append_per_sm;
     a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
     const long long l0 = g_kernel_launches;
     cudaError_t e = c->fused_append
@@ -953,6 +957,17 @@ int complete_pending(pirrt_ctx* c) {
     return c->broken ? c->kept_rc : 0;
 }
 
+// A new exploit discards an unwaited kept result -- unless that result was a
+// failure (e.g. E_NOCONV of an asynchronous exploit another call completed):
+// then the new exploit is not started and the failure is reported now.
+int take_kept_failure(pirrt_ctx* c) {
+    if (!c->kept) return 0;
+    c->kept = false;
+    if (c->kept_rc == PIRRT_OK) return 0;
+    return fail(c->kept_rc, "the previous asynchronous exploit failed (reported late; no new "
+                            "exploit was started)");
+}
+
 }  // namespace
 
 extern "C" {
@@ -962,7 +977,7 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     int rc;
     if ((rc = set_device(c))) return rc;
     if ((rc = complete_pending(c))) return rc;
-    c->kept = false;
+    if ((rc = take_kept_failure(c))) return rc;
     if ((rc = exploit_launch(c))) return rc;
     return exploit_finish(c, st);
 }
@@ -972,7 +987,7 @@ int pirrt_exploit_async(pirrt_ctx* c) {
     int rc;
     if ((rc = set_device(c))) return rc;
     if ((rc = complete_pending(c))) return rc;
-    c->kept = false;
+    if ((rc = take_kept_failure(c))) return rc;
     if ((rc = exploit_launch(c))) return rc;
     c->inflight = true;
     return PIRRT_OK;

@@ -240,6 +240,7 @@ struct AppendArgs {
     int Bcount;
     DevCtl* ctl;
     int grid_blocks;
+    int per_sm;                   // k_append_fused blocks per SM (append_blocks_per_sm)
     const int* goals;             // goal set (R4); the promising threshold of the
     int n_goals;                  // new vertices is the goal cost before the batch
 };
@@ -248,6 +249,7 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s);
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
                                 int max_blocks, const L2Window& w, cudaStream_t s);
 constexpr int kAppendMaxBlocks = 2048;
+int append_blocks_per_sm();
 
 // fold a delta CSR into its base CSR (cost arrays may be NULL: out-index)
 struct CompactArgs {

@@ -923,15 +923,21 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
 
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
                                 int max_blocks, const L2Window& w, cudaStream_t s) {
-    static int per_sm = -1;
-    if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_append_fused, kBT, 0);
-    int blocks = per_sm * (a.grid_blocks > 0 ? a.grid_blocks : 148);
+    // a.per_sm: occupancy of k_append_fused, computed once per context at
+    // pirrt_create (append_blocks_per_sm) -- device-specific, so not cached here
+    int blocks = a.per_sm * (a.grid_blocks > 0 ? a.grid_blocks : 148);
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     AppendArgs args = a;
     void* params[] = {&args, &cnt1, &bsum};
     ++g_kernel_launches;
     return launch_coop((const void*)k_append_fused, blocks, kBT, params, w, s);
+}
+
+int append_blocks_per_sm() {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_append_fused, kBT, 0);
+    return per_sm;
 }
 
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {

@@ -220,6 +220,32 @@ def _is_torch_cuda(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
 
 
+# dtype each device-pointer argument must have (the C ABI reinterprets the
+# memory: int32 ids, float64 costs / h / g / points)
+_DEV_DTYPES = {"h_new": "float64", "src": "int32", "dst": "int32", "cost": "float64",
+               "parent_new": "int32", "g_new": "float64", "points": "float64"}
+
+
+def _check_device_tensors(device: int, sizes: dict, **tensors):
+    """Device-pointer inputs: every tensor a contiguous torch CUDA tensor of
+    the ABI's dtype on the context's device, with the stated element count."""
+    for name, t in tensors.items():
+        if t is None:
+            continue
+        if not _is_torch_cuda(t):
+            raise PirrtError(PIRRT_E_INVAL, f"{name}: device-pointer append needs every input "
+                                            "as a torch CUDA tensor")
+        want = _DEV_DTYPES[name]
+        if str(t.dtype) != f"torch.{want}":
+            raise PirrtError(PIRRT_E_INVAL, f"{name}: dtype {t.dtype}, the ABI needs {want}")
+        if not t.is_contiguous():
+            raise PirrtError(PIRRT_E_INVAL, f"{name}: tensor is not contiguous")
+        if t.device.index != device:
+            raise PirrtError(PIRRT_E_INVAL, f"{name}: on {t.device}, the context is on cuda:{device}")
+        if name in sizes and int(t.numel()) != sizes[name]:
+            raise PirrtError(PIRRT_E_INVAL, f"{name}: {t.numel()} elements, expected {sizes[name]}")
+
+
 class Context:
     """One exploitation context (vertices 0 = x_init and 1 = x_goal exist)."""
 
@@ -274,10 +300,14 @@ class Context:
     def append(self, h_new, src, dst, cost, parent_new=None, g_new=None, flags=0) -> int:
         """pirrt_graph_append_batch.  numpy arrays -> host pointers; torch CUDA
         tensors (all of them) -> PIRRT_F_DEVICE_PTRS."""
-        if _is_torch_cuda(h_new) or _is_torch_cuda(src):
+        if any(_is_torch_cuda(x) for x in (h_new, src, dst, cost, parent_new, g_new)):
             flags |= PIRRT_F_DEVICE_PTRS
             ptr = lambda t: None if t is None else t.data_ptr()
             nn, m = int(h_new.numel()), int(src.numel())
+            _check_device_tensors(int(self.cfg.device),
+                                  {"dst": m, "cost": m, "parent_new": nn, "g_new": nn},
+                                  h_new=h_new, src=src, dst=dst, cost=cost,
+                                  parent_new=parent_new, g_new=g_new)
             keep = ()
         else:
             h_new = np.ascontiguousarray(h_new, np.float64)
@@ -316,6 +346,10 @@ class Context:
         nprom, ne = C.c_int32(0), C.c_int64(0)
         if _is_torch_cuda(points):
             flags |= PIRRT_F_DEVICE_PTRS
+            _check_device_tensors(int(self.cfg.device), {}, points=points)
+            if points.dim() != 2 or int(points.shape[1]) != self.d:
+                raise PirrtError(PIRRT_E_INVAL, f"points: shape {tuple(points.shape)}, "
+                                                f"expected (n, {self.d})")
             n, ptr = int(points.shape[0]), points.data_ptr()
         else:
             points = np.ascontiguousarray(points, np.float64)
