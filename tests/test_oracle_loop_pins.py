@@ -94,6 +94,24 @@ def test_r13_stalls_when_nothing_changes():
     assert o.state()[1].tolist() == [0.0, 3.0, 1.0]
 
 
+def test_r13_goes_on_after_a_parent_change_that_changes_nothing_else():
+    """Root 0 -> a=2 (c 1, h(a)=100: never expanded), a -> goal 1 (c 1),
+    0 -> goal (c 10).  Snapshot: parent(a)=0 g 1, parent(goal)=0 g 10, B={}.
+    it 1: I = {goal}: min(1+1 via a, 0+10 via 0) = 2 < 10 -> parent(goal)
+    0 -> a (a parent value CHANGED), Delta g 8.  Evaluate (thr 10): a: g 1
+    (same), f 101 -> not expanded; goal (child of a now) not visited ->
+    no g or b bit changed, but the parent did -> go on (R13 needs both).
+    it 2: goal: 2 < 10 via a again -> Delta g 8, no parent change; Evaluate
+    changes nothing -> R13 stop: iterations 2, evaluations 2, stalled 1."""
+    o = chain_oracle([0.0, 0.0, 100.0], [(0, 2, 1.0), (2, 1, 1.0), (0, 1, 10.0)],
+                     parent=[-1, 0, 0], g=[0.0, 10.0, 1.0], b=[0, 0, 0])
+    st = o.exploit()
+    assert (st.iterations, st.evaluations, st.stalled) == (2, 2, 1)
+    assert st.last_delta_g == 8.0
+    parent, g, pc, b = o.state()
+    assert parent.tolist() == [-1, 2, 0] and g.tolist() == [0.0, 10.0, 1.0]
+
+
 def eps_oracle(eps):
     """Root 0, goal 1, a=2, c=3, h = 0.  Edges 0->a 1, 0->c 0.25, c->a 0.25,
     a->goal 1, 0->goal 10.  Snapshot: parent(a)=0 g 1, parent(c)=0 g 0.25,

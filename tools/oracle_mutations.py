@@ -36,8 +36,14 @@ MUTATIONS = [
     ("Delta g as the last vertex's delta (R1 literal)", "if (d > dg) dg = d;", "dg = d;"),
     ("goal not always improved (R4)", "if (!(prune_off || c->b[v] || is_goal(c, v))) continue;",
      "if (!(prune_off || c->b[v])) continue;"),
-    ("local relaxation sees later vertices (R14)", "if (u >= v) continue;  // only vertices inserted before v",
-     "if (u == v) continue;"),
+    ("local relaxation keeps the highest id on ties (R14, R6)",
+     "if (cand < best || (cand == best && arg >= 0 && u < arg)) {",
+     "if (cand < best || (cand == best && arg >= 0 && u > arg)) {"),
+    ("new vertex promising test with <= (P:186-187)",
+     "c->b[v] = (c->g[v] + c->h[v] < thr) ? 1 : 0;", "c->b[v] = (c->g[v] + c->h[v] <= thr) ? 1 : 0;"),
+    ("Evaluate adds the parent's cost instead of the child's (R9)",
+     "c->g[v] = c->g[p] + c->pc[v];  // g(n) <- c(v,n) + g(v), P:262",
+     "c->g[v] = c->g[p] + c->pc[p];  // g(n) <- c(v,n) + g(v), P:262"),
 ]
 
 PIN_TESTS = ["tests/test_oracle_loop_pins.py", "tests/test_oracle_pins.py",
