@@ -1,21 +1,32 @@
 #!/usr/bin/env python
 """bench.py -- headline benchmark of the B200 PI-RRT# exploitation library.
 
-Workload (BASELINE.json north_star target, configs[2]): a 6-D random
-geometric graph with box obstacles and the incremental radius
-r(m) = gamma (ln m / m)^(1/6), grown by BE-RRT# batches of S samples
-(Alg. 3) to 1,000,000 vertices.  One STEP is one pass of
-the whole hot path over one batch:
-pirrt_graph_append_batch (a1, incl. local relaxation) -> pirrt_exploit
-(a2-a5, converged policy iteration; skipped only by the Alg. 3 guard) ->
-pirrt_best_path (a6).  The device leg (`value`) times the W warm-up + K timed
-batches that end exactly at vertex 1,000,000, with the batch inputs already
-resident in HBM; the e2e leg times the next W + K batches through the same
+Metric (BASELINE.json): ms per converged PI exploitation + edge relaxations/s
+(GTEPS) vs the gather roofline.
+
+N = 1 (default), BASELINE.json configs[2]: a 6-D random geometric graph with
+box obstacles and the incremental radius r(m) = gamma (ln m / m)^(1/6),
+grown by BE-RRT# batches of S samples (Alg. 3) to
+1,000,000 vertices.  One STEP is one pass of the whole hot path (SURVEY.md
+section 8(a) rows a1-a6) over one batch: pirrt_graph_append_batch (a1, incl.
+the local relaxation) -> pirrt_exploit (a2-a5, converged policy iteration;
+skipped only by the Alg. 3 guard) -> pirrt_best_path (a6).  `value` times the
+W warm-up + K timed batches that end exactly at vertex 1,000,000 with the
+batch inputs resident in HBM; `e2e` times the next batches through the same
 C ABI from pinned HOST buffers (H2D/D2H inside the timed region).
+Sub-records of the same run:
+  gamma_star  configs[2] at SURVEY.md's headline radius gamma* (mean degree
+              ~1,140), built by the device-side Extend: per-batch exploits at
+              S = 4096 and 65536 (the 10 batches ending at n) and the cold
+              solve (S = N) -- the HBM-bound case, with its own roofline;
+  config2     configs[1]: 2-D 50k clutter, S = 1 (tight sync), per replan;
+  cpu_baseline  the serial oracle on ONE pinned host core, on the identical
+              state (the GPU's state at the start of the timed batches is
+              handed to it: SURVEY.md 8(d)), timed on the same batches.
+N > 1 (`--gpus N` spawns torchrun itself; or under torchrun): configs[4],
+the 10M-vertex 6-D gamma_k RRG sharded over the ranks (strong scaling).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
-Under torchrun (N > 1) every rank runs an independent replica (weak scaling,
-DESIGN.md section 7); timing is the max over ranks.
 """
 from __future__ import annotations
 
@@ -35,16 +46,19 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ms per converged PI exploitation + edge relaxations/s (GTEPS) vs gather roofline"
 
-# algorithmic bytes per unit of work
+# Algorithmic bytes per unit of work:
 B_RELAX = 20.0      # Improve relaxation: idx i32 + cost f64 streamed (12 B) + g[u] gather (8 B)
 B_IVERT = 40.0      # Improve vertex: 4 row offsets (32 B) + g[v] (8 B)
-B_SCAN = 8.0        # Evaluate out-row entry: idx i32 (4 B) + parent[c] gather (4 B)
-B_VISIT = 38.0      # Evaluate child visit: stamp 4, pc 8, g read 8, g write 8, h 8, b 2
+B_VISIT = 37.0      # Evaluate visit: parent 4, pc 8, g[p] 8, g write 8, h 8, b 1
+ALGO_FORMULA = "20 B x relaxations + 40 B x improve_set + 37 B x eval_work (SURVEY.md 8(d) units)"
 
 
-def algo_bytes(st, n):
-    return (st.relaxations * B_RELAX + st.improve_set * B_IVERT + st.eval_scanned * B_SCAN
-            + st.eval_visits * B_VISIT)
+def algo_bytes(st) -> float:
+    """Bytes the launch's algorithm must move: every relaxation and Improve
+    vertex it processes, every child it visits (eval_work: an incremental
+    Evaluate visits only the changed subtrees).  Out-row entries scanned to
+    find children are implementation overhead, reported apart."""
+    return st.relaxations * B_RELAX + st.improve_set * B_IVERT + st.eval_work * B_VISIT
 
 
 def parse():
@@ -53,69 +67,81 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
+    ap.add_argument("--workload", choices=["auto", "cfg3", "cfg5"], default="auto",
+                    help="auto: cfg3 at N = 1, cfg5 (10M sharded) at N > 1")
     ap.add_argument("--d", type=int, default=6)
-    ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--S", type=int, default=4096)
+    ap.add_argument("--n", type=int, default=0, help="vertices (default: 1M cfg3, 10M cfg5)")
+    ap.add_argument("--S", type=int, default=0, help="batch (default: 4096 cfg3, 65536 cfg5)")
     ap.add_argument("--gamma", choices=["k", "star"], default="k")
     ap.add_argument("--boxes", type=int, default=20)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the gamma* and config-2 records")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graph-cache", default="", help="npz path to reuse a generated graph")
     ap.add_argument("--grid-blocks", type=int, default=0,
                     help="persistent exploit grid (0 = SMs x occupancy)")
-    ap.add_argument("--sharded", action="store_true",
-                    help="one graph split over the ranks (NCCL sharded exploit, strong scaling) "
-                         "instead of independent replicas (weak scaling)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    return a
+
+
+def resolve(a, world):
+    if a.workload == "auto":
+        a.workload = "cfg3" if world == 1 else "cfg5"
+    if a.workload == "cfg3":
+        a.n = a.n or 1_000_000
+        a.S = a.S or 4096
+    else:
+        a.n = a.n or 10_000_000
+        a.S = a.S or 65536
+        a.gamma = "k"
+    return a
 
 
 def workload_name(a):
+    if a.workload == "cfg5":
+        return f"cfg5_{a.d}d_{a.n // 1000}k_sharded_S{a.S}_gamma{a.gamma}_{a.boxes}boxes"
     return f"cfg3_{a.d}d_{a.n // 1000}k_berrt_S{a.S}_gamma{a.gamma}_{a.boxes}boxes"
+
+
+def spawn_if_needed(a):
+    """`--gpus N` (N > 1) outside torchrun: relaunch under torch.distributed.run
+    with one rank per GPU (127.0.0.1 rendezvous), exit with its status."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 # ------------------------------------------------------------------ inputs
 
-def make_graph(a, rank, world):
-    """Generate (rank 0) or load (other ranks) the seeded RRG."""
+def make_graph(a, rank, world, seed_name=None):
+    """Generate (rank 0) or load (other ranks) the seeded RRG (CPU generator)."""
     import gen
     gm = gen.gamma_k(a.d) if a.gamma == "k" else gen.gamma_star(a.d)
     n_total = a.n + 2 * (a.warmup + a.steps) * a.S
-    seed = gen.seed_of(workload_name(a), a.seed)
-    shm = f"/dev/shm/pirrt_bench_{os.getpid() if world == 1 else os.environ.get('MASTER_PORT', '0')}.npz"
+    seed = gen.seed_of(seed_name or workload_name(a), a.seed)
     t0 = time.perf_counter()
-    cache = a.graph_cache
     g = None
-    if cache and os.path.exists(cache) and (world == 1 or rank == 0):
+    if a.graph_cache and os.path.exists(a.graph_cache):
         # the generator is prefix-stable (vertex i's edges depend only on
         # points <= i), so a cached graph with at least n_total vertices serves
-        z = np.load(cache)
+        z = np.load(a.graph_cache)
         if int(z["meta"][2]) == seed and int(z["h"].size) >= n_total:
             g = gen.RRG(a.d, int(z["h"].size), gm, z["points"], z["boxes"], z["h"], z["off"],
                         z["nbr"], z["cost"], int(z["meta"][0]), int(z["meta"][1]))
-    if g is None and (world == 1 or rank == 0):
-        threads = max(1, (os.cpu_count() or 1))
-        g = gen.rrg(a.d, n_total, gm, n_boxes=a.boxes, seed=seed, threads=threads)
-        if cache:
-            np.savez(cache, points=g.points, boxes=g.boxes, h=g.h, off=g.off, nbr=g.nbr,
+    if g is None:
+        g = gen.rrg(a.d, n_total, gm, n_boxes=a.boxes, seed=seed, threads=max(1, os.cpu_count() or 1))
+        if a.graph_cache:
+            np.savez(a.graph_cache, points=g.points, boxes=g.boxes, h=g.h, off=g.off, nbr=g.nbr,
                      cost=g.cost, meta=np.array([g.n_isolated, g.n_candidates, seed], np.uint64))
-    if world == 1 or rank == 0:
-        if world > 1:
-            np.savez(shm, points=g.points, boxes=g.boxes, h=g.h, off=g.off, nbr=g.nbr,
-                     cost=g.cost, meta=np.array([g.n_isolated, g.n_candidates]))
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        if rank != 0:
-            z = np.load(shm)
-            g = gen.RRG(a.d, n_total, gm, z["points"], z["boxes"], z["h"], z["off"], z["nbr"],
-                        z["cost"], int(z["meta"][0]), int(z["meta"][1]))
-        dist.barrier()
-        if rank == 0:
-            try:
-                os.unlink(shm)
-            except OSError:
-                pass
     return g, gm, time.perf_counter() - t0
 
 
@@ -139,7 +165,7 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.proc = None
-        self.path = f"/tmp/pirrt_clocks_{os.getpid()}.csv"
+        self.path = f"/tmp/pirrt_clocks_{os.getpid()}_{device}.csv"
 
     def start(self):
         try:
@@ -184,31 +210,72 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-# ------------------------------------------------------------------ legs
+def stats_summary(xs, nd=4):
+    xs = sorted(float(x) for x in xs)
+    if not xs:
+        return None
+    m = statistics.mean(xs)
+    return {"median": round(statistics.median(xs), nd),
+            "p95": round(xs[min(len(xs) - 1, int(round(0.95 * (len(xs) - 1))))], nd),
+            "mean": round(m, nd), "std": round(statistics.pstdev(xs), nd),
+            "min": round(xs[0], nd), "max": round(xs[-1], nd), "count": len(xs)}
 
-def run_cuda(a, rank, world):
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    """DRAM bytes per exploit_kernel launch from the committed ncu --set full
+    capture of this bench command (profiles/r2/exploit_ncu.json), if it was
+    taken on this workload; else None."""
+    try:
+        p = json.load(open(os.path.join(ROOT, "profiles", "r2", "exploit_ncu.json")))
+        if p.get("workload") == workload:
+            return p.get("dram_bytes_per_launch"), p.get("source")
+    except Exception:
+        pass
+    return None, None
+
+
+def counters(ex):
+    """Sums of the exploit stats over a list of exploits."""
+    keys = ("relaxations", "improve_set", "eval_visits", "eval_work", "eval_scanned", "iterations",
+            "evaluations", "full_evaluations", "inc_evaluations", "barriers")
+    return {k: int(sum(getattr(s, k) for s in ex)) for k in keys}
+
+
+def roofline_of(ex, peak, peak_src, kernel):
+    ms = sum(s.device_ms for s in ex)
+    byt = sum(algo_bytes(s) for s in ex)
+    ach = byt / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    return {"kernel": kernel, "bound": "hbm", "achieved": round(ach, 2), "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 5),
+            "algorithmic_bytes_per_launch": round(byt / max(1, len(ex))),
+            "formula": ALGO_FORMULA}
+
+
+# ------------------------------------------------------------------ N = 1: configs[2]
+
+def run_cuda(a, dev):
     import torch
     from paper_2003_04920_b200 import pirrt
     from paper_2003_04920_b200.berrt import EDGES_UNDIRECTED, replay
 
-    dev = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(dev)
-    g, gm, t_gen = make_graph(a, rank, world)
+    g, gm, t_gen = make_graph(a, 0, 1)
     dev0, dev_batches, e2e_batches = legs(a)
     stream = torch.cuda.current_stream()
-    shard_kw = {}
-    if a.sharded:
-        from paper_2003_04920_b200 import dist as pdist
-        nid = pdist.broadcast_unique_id(pirrt.nccl_unique_id) if world > 1 else None
-        shard_kw = dict(nranks=world, rank=rank, nccl_id=nid,
-                        flags=pirrt.PIRRT_F_SHARDED if world == 1 else 0)
     ctx = pirrt.Context(h_root=g.h_root(), stream=stream, vertex_capacity=g.n + 1024,
-                        edge_capacity=int(2.4 * g.off[-1]) + 4096, grid_blocks=a.grid_blocks,
-                        **shard_kw)
+                        edge_capacity=int(2.4 * g.off[-1]) + 4096, grid_blocks=a.grid_blocks)
     # ---- pre-load: BE-RRT# history up to dev0 (untimed)
     t0 = time.perf_counter()
     replay(ctx, g, a.S, n_stop=dev0, final=False)
     t_pre = time.perf_counter() - t0
+    snap = ctx.state()                     # hand-off state for the cpu_baseline (SURVEY.md 8(d))
     # ---- inputs of the device leg resident in HBM before timing
     def to_dev(x):
         return torch.from_numpy(np.ascontiguousarray(x)).to(f"cuda:{dev}")
@@ -232,13 +299,9 @@ def run_cuda(a, rank, world):
     for i in range(a.warmup):
         flush.zero_()
         step(dev_in[i])
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
     torch.cuda.synchronize()
     l0 = ctx.kernel_launches
     torch.cuda.nvtx.range_push("timed")
-    wall0 = time.perf_counter()
     for i in range(a.warmup, a.warmup + a.steps):
         flush.zero_()                                          # L2 flush between timed steps
         e0, e1 = ev[i]
@@ -247,15 +310,9 @@ def run_cuda(a, rank, world):
         e1.record(stream)
         stats.append(st)
     torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
     torch.cuda.nvtx.range_pop()
     launches = ctx.kernel_launches - l0
     step_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(a.warmup, a.warmup + a.steps)]
-    if os.environ.get("PIRRT_BENCH_VERBOSE"):
-        for i, (ms, st) in enumerate(zip(step_ms, stats)):
-            print(f"dev step {i}: {ms:.3f} ms exploit={st.device_ms if st else 0:.3f} "
-                  f"it={st.iterations if st else 0}", file=sys.stderr, flush=True)
-    total_ms = float(sum(step_ms))
     # ---- e2e leg: same ABI from pinned host buffers
     host_in = []
     for (lo, hi) in e2e_batches:
@@ -272,12 +329,9 @@ def run_cuda(a, rank, world):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        st, nprom, path = step(host_in[i])
+        step(host_in[i])
         e1.record(stream)
         torch.cuda.synchronize()
-        if os.environ.get("PIRRT_BENCH_VERBOSE"):
-            print(f"e2e step {i}: {e0.elapsed_time(e1):.3f} ms edges={ctx.n_edges} "
-                  f"exploit={st.device_ms if st else 0:.3f}", file=sys.stderr, flush=True)
         if i >= a.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
     # (b) pipelined through the asynchronous exploit:
@@ -318,143 +372,223 @@ def run_cuda(a, rank, world):
     e2e_pipe_ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     ex = [s for s in stats if s is not None]
-    relax = sum(s.relaxations for s in ex)
-    ex_ms = sum(s.device_ms for s in ex)
-    bytes_ = sum(algo_bytes(s, a.n) for s in ex)
     res = {
-        "total_ms": total_ms, "step_ms": step_ms, "wall_s": wall, "launches": launches,
-        "relax": relax, "exploit_ms": ex_ms, "bytes": bytes_, "n_exploits": len(ex),
+        "step_ms": step_ms, "launches": launches, "ex": ex, "n_exploits": len(ex),
+        "relax_per_step": [s.relaxations if s else 0 for s in stats],
         "e2e_ms": float(e2e_pipe_ms), "e2e_sync_ms": float(sum(e2e_ms)),
         "e2e_sync_steps": len(e2e_ms), "h2d": h2d / a.steps, "d2h": d2h / a.steps,
         "clocks": clk, "t_gen": t_gen, "t_pre": t_pre,
-        "iters": [s.iterations for s in ex], "prom": [s.promising for s in ex],
-        "exploit_ms_list": [s.device_ms for s in ex],
-        "improve_ms": sum(s.improve_ms for s in ex), "evaluate_ms": sum(s.evaluate_ms for s in ex),
-        "barriers": sum(s.barriers for s in ex),
-        "improve_bytes": sum(s.relaxations * B_RELAX + s.improve_set * B_IVERT for s in ex),
-        "max_level": max([s.max_level for s in ex] or [0]),
         "graph": {"n_total": g.n, "pairs": g.n_pairs, "mean_degree": g.mean_degree,
                   "isolated": g.n_isolated, "gamma": gm},
-        "edges_stored": ctx.n_edges, "n_at_end_of_device_leg": a.n,
+        "edges_stored": ctx.n_edges, "snap": snap,
     }
+    del ctx, dev_in, flush
+    torch.cuda.empty_cache()
     return res, g, gm
 
 
-def oracle_leg(a, g, batches, budget_s, p0):
-    """Time the serial oracle on a bounded sample of the same workload.
-
-    The oracle builds its own state (no input from the CUDA path): vertices
-    [2, p0) appended as one batch and exploited (untimed), then the given
-    S-batches are timed one by one (append + exploit + best_path) until the
-    budget is spent."""
-    from oracle import EDGES_UNDIRECTED, Oracle
-    o = Oracle(h_root=g.h_root())
+def gamma_star_record(a, peak, peak_src, K=10):
+    """configs[2] at gamma* (SURVEY.md 8(d) headline radius), graph built on
+    the device (pirrt_extend_batch, NEXT-2) from the generator's samples:
+    per-batch exploits of the K batches ending at n for S = 4096 and 65536,
+    and the cold solve (every vertex appended with no exploit in between --
+    bit-identical to one S = N append -- then one exploit)."""
+    import torch
+    import gen
+    from paper_2003_04920_b200 import pirrt
+    d, n, boxes = a.d, a.n, a.boxes
+    gm = gen.gamma_star(d)
     t0 = time.perf_counter()
-    s, d_, c = g.batch(2, p0, directed=False)
-    o.append(g.h[2:p0], s, d_, c, flags=EDGES_UNDIRECTED)
-    o.exploit()
+    pts, bx = gen.points(d, n, boxes, seed=gen.seed_of("cfg3_gstar", d, n, boxes, a.seed))
+    h_root = float(np.sqrt(((pts[0] - pts[1]) ** 2).sum()))
+    dpts = torch.from_numpy(pts).cuda()
+    rec = {"gamma_value": round(gm, 6), "sampling_s": round(time.perf_counter() - t0, 2)}
+    ecap = int(2.2 * 600 * n)
+
+    def fresh():
+        c = pirrt.Context(h_root=h_root, stream=torch.cuda.current_stream(),
+                          vertex_capacity=n + 1024, edge_capacity=ecap)
+        c.set_world(d, bx, pts[0], pts[1], gm)
+        return c
+
+    for S in (4096, 65536):
+        t0 = time.perf_counter()
+        ctx = fresh()
+        lo, stop = 2, n - K * S
+        while lo < stop:
+            hi = min(stop, lo + S)
+            if ctx.extend(dpts[lo:hi])[0] > 0:
+                ctx.exploit()
+            lo = hi
+        ex, ext_ms = [], []
+        for k in range(K):
+            hi = lo + S
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            nprom, _ = ctx.extend(dpts[lo:hi])
+            ext_ms.append(1e3 * (time.perf_counter() - t1))
+            if nprom > 0:
+                ex.append(ctx.exploit())
+            lo = hi
+        c = counters(ex)
+        rec[f"S{S}"] = {
+            "batches_timed": K, "exploits": len(ex),
+            "exploit_ms": stats_summary([s.device_ms for s in ex]),
+            "extend_plus_append_ms_host": stats_summary(ext_ms),
+            "iterations_mean": round(c["iterations"] / max(1, len(ex)), 3),
+            "promising_mean": round(statistics.mean([s.promising for s in ex]), 1) if ex else 0,
+            "gteps": round(c["relaxations"] / (sum(s.device_ms for s in ex) * 1e-3) / 1e9, 3) if ex else 0,
+            "counters": c, "roofline": roofline_of(ex, peak, peak_src, "exploit_kernel (per batch)"),
+            "mean_degree": round(ctx.n_edges / ctx.n, 2), "setup_s": round(time.perf_counter() - t0, 1)}
+        del ctx
+        torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    ctx = fresh()
+    for lo in range(2, n, 131072):
+        ctx.extend(dpts[lo:min(n, lo + 131072)])
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    st = ctx.exploit()
+    rec["cold"] = {"exploit_ms": round(st.device_ms, 4), "iterations": st.iterations,
+                   "evaluations": st.evaluations, "improve_ms": round(st.improve_ms, 4),
+                   "evaluate_ms": round(st.evaluate_ms, 4),
+                   "gteps": round(st.relaxations / (st.device_ms * 1e-3) / 1e9, 3),
+                   "counters": counters([st]), "directed_edges": ctx.n_edges,
+                   "mean_degree": round(ctx.n_edges / ctx.n, 2), "build_s": round(t_build, 2),
+                   "roofline": roofline_of([st], peak, peak_src,
+                                           "exploit_kernel + improve_wide_kernel (cold solve)")}
+    del ctx, dpts
+    torch.cuda.empty_cache()
+    return rec
+
+
+def config2_record(a, n=50_000, boxes=30):
+    """configs[1]: 2-D 50k clutter (30 boxes, gamma*), S = 1 (PI-RRT#, tight
+    sync): one append + (guarded) exploit per sample; per-replan exploit times."""
+    import torch
+    import gen
+    from paper_2003_04920_b200 import pirrt
+    gm = gen.gamma_star(2)
+    t0 = time.perf_counter()
+    g = gen.rrg(2, n, gm, n_boxes=boxes, seed=gen.seed_of("cfg2_2d_50k_S1_gammastar", boxes, a.seed),
+                threads=max(1, os.cpu_count() or 1))
+    t_gen = time.perf_counter() - t0
+    ctx = pirrt.Context(h_root=g.h_root(), stream=torch.cuda.current_stream(),
+                        vertex_capacity=n + 1024, edge_capacity=int(2.4 * g.off[-1]) + 4096)
+    ex, host = [], []
+    t0 = time.perf_counter()
+    for v in range(2, n):
+        s, d_, c = g.batch(v, v + 1, directed=False)
+        if ctx.append(g.h[v:v + 1], s, d_, c, flags=pirrt.PIRRT_F_EDGES_UNDIRECTED) > 0:
+            t1 = time.perf_counter()
+            ex.append(ctx.exploit())
+            host.append(1e3 * (time.perf_counter() - t1))
+    t_run = time.perf_counter() - t0
+    c = counters(ex)
+    out = {"workload": "cfg2_2d_50k_S1_gammastar_30boxes", "replans": len(ex),
+           "exploit_ms": stats_summary([s.device_ms for s in ex]),
+           "exploit_host_ms": stats_summary(host),
+           "iterations_mean": round(c["iterations"] / max(1, len(ex)), 3),
+           "exploit_ms_total": round(sum(s.device_ms for s in ex), 2),
+           "counters": c, "mean_degree": round(g.mean_degree, 2), "generate_s": round(t_gen, 2),
+           "run_s": round(t_run, 2)}
+    del ctx
+    return out
+
+
+def cpu_baseline_handoff(a, g, snap, budget_s, gpu_relax):
+    """The serial oracle on ONE pinned host core, on the identical state: the
+    GPU's state at dev0 is handed over (graph [0, dev0) appended, then
+    set_policy), then the same batches as the GPU's timed steps are run
+    (append + exploit + best_path) until the budget is spent."""
+    from oracle import EDGES_UNDIRECTED, Oracle
+    dev0, dev_batches, _ = legs(a)
+    parent, gg, _, b = snap
+    t0 = time.perf_counter()
+    o = Oracle(h_root=g.h_root())
+    s, d_, c = g.batch(2, dev0, directed=False)
+    o.append(g.h[2:dev0], s, d_, c, flags=EDGES_UNDIRECTED)
+    o.set_policy(parent, gg, b)
     t_setup = time.perf_counter() - t0
-    times, relax = [], 0
-    spent = 0.0
-    for (lo, hi) in batches:
-        s, d_, c = g.batch(lo, hi, directed=False)
-        t = time.perf_counter()
-        nprom = o.append(g.h[lo:hi], s, d_, c, flags=EDGES_UNDIRECTED)
-        st = o.exploit() if nprom > 0 else None
-        o.best_path()
-        dt = time.perf_counter() - t
-        times.append(dt)
-        relax += st.relaxations if st else 0
-        spent += dt
-        if spent > budget_s:
-            break
-    return times, relax, t_setup
+    cores = os.cpu_count()
+    mask = None
+    try:
+        mask = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(mask)})
+    except (AttributeError, OSError):
+        pass
+    times, relax, spent = [], [], 0.0
+    try:
+        for i, (lo, hi) in enumerate(dev_batches):
+            s, d_, c = g.batch(lo, hi, directed=False)
+            t = time.perf_counter()
+            nprom = o.append(g.h[lo:hi], s, d_, c, flags=EDGES_UNDIRECTED)
+            st = o.exploit() if nprom > 0 else None
+            o.best_path()
+            dt = time.perf_counter() - t
+            relax.append(st.relaxations if st else 0)
+            if i >= a.warmup:
+                times.append(dt)
+                spent += dt
+                if spent > budget_s:
+                    break
+    finally:
+        if mask:
+            os.sched_setaffinity(0, mask)
+    k = len(times)
+    gpu_same = gpu_relax[:k]
+    model = cpu_model()
+    return {
+        "value": round(1e3 * statistics.mean(times), 3) if times else None, "unit": "ms",
+        "cores": 1, "kind": "oracle",
+        "sample": f"{k} of the {a.steps} timed S={a.S} steps (append + exploit + best_path), "
+                  f"same batches as the GPU, on the GPU's state at n={dev0} handed over "
+                  f"(append + set_policy, {t_setup:.1f}s untimed); serial oracle pinned to 1 of "
+                  f"{cores} host cores ({model})",
+        "relaxations_per_step": {"oracle": relax[a.warmup:a.warmup + k], "gpu": gpu_same,
+                                 "equal": relax[a.warmup:a.warmup + k] == gpu_same},
+    }
 
 
-def cpu_info():
-    model = "unknown"
+def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
             if line.startswith("model name"):
-                model = line.split(":", 1)[1].strip()
-                break
+                return line.split(":", 1)[1].strip()
     except OSError:
         pass
-    return model, os.cpu_count()
+    return "unknown"
 
 
-def step_stats(xs):
-    xs = sorted(float(x) for x in xs)
-    if not xs:
-        return None
-    m = statistics.mean(xs)
-    return {"median": round(statistics.median(xs), 4),
-            "p95": round(xs[min(len(xs) - 1, int(round(0.95 * (len(xs) - 1))))], 4),
-            "mean": round(m, 4), "std": round(statistics.pstdev(xs), 4),
-            "min": round(xs[0], 4), "max": round(xs[-1], 4)}
-
-
-def peaks():
-    try:
-        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
-
-
-def traffic_per_launch():
-    p = os.path.join(ROOT, "profiles", "exploit_ncu_summary.json")
-    try:
-        return json.load(open(p)).get("dram_bytes_per_launch")
-    except Exception:
-        return None
-
-
-def main():
-    a = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if a.impl == "reference":
-        return main_reference(a, rank, world)
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
-    res, g, gm = run_cuda(a, rank, world)
-    total_ms, relax, e2e_ms = res["total_ms"], res["relax"], res["e2e_ms"]
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        r = torch.tensor([float(relax)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(r, op=dist.ReduceOp.SUM)
-        total_ms, e2e_ms, relax_all = float(t[0]), float(t[1]), float(r[0])
-    else:
-        relax_all = float(relax)
-    if rank != 0:
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-            dist.destroy_process_group()
-        return
-    ms_step = total_ms / a.steps
+def main_cuda_single(a):
+    import torch
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
     peak, peak_src = peaks()
-    achieved = res["bytes"] / (res["exploit_ms"] * 1e-3) / 1e9 if res["exploit_ms"] > 0 else 0.0
+    res, g, gm = run_cuda(a, dev)
+    ex = res["ex"]
+    total_ms = float(sum(res["step_ms"]))
+    ms_step = total_ms / a.steps
+    c = counters(ex)
+    ex_ms = sum(s.device_ms for s in ex)
+    rl = roofline_of(ex, peak, peak_src,
+                     "exploit_kernel (persistent cooperative: Improve + Evaluate, all iterations)")
+    traffic, tsrc = ncu_traffic(workload_name(a))
+    rl["traffic"] = traffic
+    rl["traffic_source"] = tsrc
+    imp_ms = sum(s.improve_ms for s in ex)
     line = {
         "metric": METRIC,
         "value": round(ms_step, 4),
         "unit": "ms",
-        "n_gpus": world,
+        "n_gpus": 1,
         "steps": a.steps,
         "warmup": a.warmup,
         "ms_per_step": round(ms_step, 4),
-        # per-step distribution on this rank (P:498-499 report trials; SURVEY.md 8(d))
-        "step_ms_stats": step_stats(res["step_ms"]),
-        "exploit_ms_stats": step_stats(res["exploit_ms_list"]),
+        "step_ms_stats": stats_summary(res["step_ms"]),
+        "exploit_ms_stats": stats_summary([s.device_ms for s in ex]),
         "higher_is_better": False,
-        "scaling": "strong" if a.sharded else "weak",
+        "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
@@ -465,34 +599,23 @@ def main():
             "directed_edges_stored": res["edges_stored"],
             "step": "append(S, device ptrs) + exploit-to-convergence + best_path",
             "l2": "flushed between timed steps (256 MiB write)",
-            "parallelism": (f"sharded{world}" if a.sharded else
-                            ("single" if world == 1 else f"replicas{world}")),
+            "parallelism": "single",
         },
-        "gteps": round(relax_all / (total_ms * 1e-3) / 1e9, 4),
-        "exploit_ms_mean": round(res["exploit_ms"] / max(1, res["n_exploits"]), 4),
-        "exploit_gteps": round(res["relax"] / (res["exploit_ms"] * 1e-3) / 1e9, 4) if res["exploit_ms"] else 0,
-        "append_plus_readout_ms_mean": round((res["total_ms"] - res["exploit_ms"]) / a.steps, 4),
-        "iterations_mean": round(statistics.mean(res["iters"]), 3) if res["iters"] else 0,
-        "promising_mean": round(statistics.mean(res["prom"]), 1) if res["prom"] else 0,
-        "relaxations_per_step": round(res["relax"] / a.steps),
-        "max_level": res["max_level"],
-        "phase_ms": {"improve": round(res["improve_ms"], 4),
-                     "evaluate": round(res["evaluate_ms"], 4)},
-        "grid_barriers_per_exploit": round(res["barriers"] / max(1, res["n_exploits"]), 1),
-        "roofline": {
-            "kernel": "exploit_kernel (persistent cooperative: Improve + Evaluate, all iterations)",
-            "bound": "hbm",
-            "achieved": round(achieved, 2),
-            "peak": peak,
-            "peak_source": peak_src,
-            "unit": "GB/s",
-            "frac": round(achieved / peak, 5),
-            "traffic": traffic_per_launch(),
-            "algorithmic_bytes_per_launch": round(res["bytes"] / max(1, res["n_exploits"])),
-            "improve_phase_GBps": round(res["improve_bytes"] / (res["improve_ms"] * 1e-3) / 1e9, 2)
-            if res["improve_ms"] > 0 else None,
-        },
-        "e2e": {"value": round(e2e_ms / a.steps, 4), "unit": "ms",
+        "gteps": round(c["relaxations"] / (total_ms * 1e-3) / 1e9, 4),
+        "exploit_ms_mean": round(ex_ms / max(1, len(ex)), 4),
+        "exploit_gteps": round(c["relaxations"] / (ex_ms * 1e-3) / 1e9, 4) if ex_ms else 0,
+        "append_plus_readout_ms_mean": round((total_ms - ex_ms) / a.steps, 4),
+        "iterations_mean": round(c["iterations"] / max(1, len(ex)), 3),
+        "promising_mean": round(statistics.mean([s.promising for s in ex]), 1) if ex else 0,
+        "relaxations_per_step": round(c["relaxations"] / a.steps),
+        "counters": c,
+        "max_level": max([s.max_level for s in ex] or [0]),
+        "phase_ms": {"improve": round(imp_ms, 4), "evaluate": round(sum(s.evaluate_ms for s in ex), 4)},
+        "grid_barriers_per_exploit": round(c["barriers"] / max(1, len(ex)), 1),
+        "roofline": rl,
+        "overhead": {"eval_scanned_entries": c["eval_scanned"],
+                     "note": "out-row entries scanned to find children (8 B each), not a 8(d) unit"},
+        "e2e": {"value": round(res["e2e_ms"] / a.steps, 4), "unit": "ms",
                 "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"]),
                 "mode": "pipelined: append of batch k+1 (H2D from pinned host) overlaps the "
                         "asynchronous exploit of batch k (pirrt_exploit_async); per step one "
@@ -502,69 +625,200 @@ def main():
         "clocks": res["clocks"],
         "setup_s": {"generate": round(res["t_gen"], 2), "preload_replay": round(res["t_pre"], 2)},
     }
-    if world == 1 and not a.no_cpu_baseline:
-        dev0, dev_batches, _ = legs(a)
-        times, orelax, t_setup = oracle_leg(a, g, dev_batches, a.cpu_budget_s, dev0)
-        model, ncpu = cpu_info()
-        line["cpu_baseline"] = {
-            "value": round(1e3 * statistics.mean(times), 3), "unit": "ms", "cores": 1,
-            "kind": "oracle",
-            "sample": f"{len(times)} S={a.S} steps (append+exploit+best_path) of the same graph "
-                      f"after the oracle built its own state at n={dev0} (one batch + exploit, "
-                      f"{t_setup:.1f}s untimed); serial oracle on 1 of {ncpu} host cores ({model})",
-        }
+    if not a.no_extras:
+        line["gamma_star"] = gamma_star_record(a, peak, peak_src)
+        line["config2"] = config2_record(a)
+    if not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_handoff(a, g, res["snap"], a.cpu_budget_s,
+                                                    res["relax_per_step"])
     else:
         line["cpu_baseline"] = None
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ N > 1: configs[4]
+
+def main_sharded(a, rank, world):
+    """configs[4]: the 10M-vertex 6-D gamma_k RRG, every rank building the
+    same graph with the device-side Extend (replicated store), exploits
+    sharded over the ranks (Improve split by vertex, NCCL all-gather of the
+    records per PI iteration, replicated Evaluate).
+    Step = one S-batch extend + exploit; the cold solve is a sub-record."""
+    import torch
+    import torch.distributed as dist
+    import gen
+    from paper_2003_04920_b200 import pirrt
+    from paper_2003_04920_b200 import dist as pdist
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
     if world > 1:
-        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        nid = pdist.broadcast_unique_id(pirrt.nccl_unique_id)
+        kw = dict(nranks=world, rank=rank, nccl_id=nid)
+    else:
+        kw = {}
+    d, n, S, W, K = a.d, a.n, a.S, a.warmup, a.steps
+    gm = gen.gamma_k(d)
+    n_all = n + (W + K) * S
+    pts, bx = gen.points(d, n_all, a.boxes, seed=gen.seed_of(workload_name(a), a.seed))
+    h_root = float(np.sqrt(((pts[0] - pts[1]) ** 2).sum()))
+    dpts = torch.from_numpy(pts).cuda()
+    ctx = pirrt.Context(h_root=h_root, stream=torch.cuda.current_stream(), vertex_capacity=n_all + 1024,
+                        edge_capacity=int(2.2 * 45 * n_all), **kw)
+    ctx.set_world(d, bx, pts[0], pts[1], gm)
+    t0 = time.perf_counter()
+    for lo in range(2, n, S):
+        ctx.extend(dpts[lo:min(n, lo + S)])
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier()
+    cold = ctx.exploit()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(W + K)]
+    stats = []
+    lo = n
+    for i in range(W + K):
+        if i == W:
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+        hi = lo + S
+        ev[i][0].record()
+        nprom, _ = ctx.extend(dpts[lo:hi])
+        st = ctx.exploit() if nprom > 0 else None
+        ev[i][1].record()
+        if i >= W:
+            stats.append(st)
+        lo = hi
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(W, W + K)]
+    t = torch.tensor([sum(step_ms), cold.device_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)          # max over ranks
+    total_ms, cold_ms = float(t[0]), float(t[1])
+    ex = [s for s in stats if s is not None]
+    if rank == 0:
+        peak, peak_src = peaks()
+        relax_all = sum(s.relaxations for s in ex)          # rank shares summed below
+        r = torch.tensor([float(relax_all), float(cold.relaxations)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(r, op=dist.ReduceOp.SUM)
+    else:
+        r = torch.tensor([float(sum(s.relaxations for s in ex)), float(cold.relaxations)],
+                         dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(r, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        ms_step = total_ms / K
+        line = {
+            "metric": METRIC, "value": round(ms_step, 4), "unit": "ms", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": round(ms_step, 4),
+            "step_ms_stats": stats_summary(step_ms), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(a), "d": d, "n": n, "S": S, "gamma": "k",
+                       "gamma_value": round(gm, 6), "boxes": a.boxes,
+                       "directed_edges_stored": ctx.n_edges,
+                       "step": "extend(S points, device) + exploit-to-convergence (sharded)",
+                       "parallelism": f"sharded{world}" if world > 1 else "single"},
+            "gteps": round(float(r[0]) / (total_ms * 1e-3) / 1e9, 4),
+            "cold_solve": {"exploit_ms": round(cold_ms, 4), "iterations": cold.iterations,
+                           "gteps": round(float(r[1]) / (cold_ms * 1e-3) / 1e9, 3)},
+            "build_s": round(t_build, 2), "clocks": clk, "cpu_baseline": None,
+            "e2e": None, "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ reference arm
+
 def main_reference(a, rank, world):
-    """--impl reference: the oracle (the only reference this tier has), timed
-    on the host cores on the same workload; rank 0 only."""
+    """--impl reference: the oracle (the only reference this tier has), as it
+    stands, on one pinned host core; it replays the same BE-RRT# trajectory
+    (S-batches from vertex 2, Alg. 3 guard) untimed up to the timed batches,
+    so its state and work per step equal the GPU arm's.  Rank 0 only."""
     if rank != 0:
         return
-    g, gm, _ = make_graph(a, 0, 1)
-    dev0, dev_batches, _ = legs(a)
     from oracle import EDGES_UNDIRECTED, Oracle
+    from paper_2003_04920_b200.berrt import batches
+    a = resolve(a, world)
+    name = workload_name(a)
+    sample = ""
+    if a.workload == "cfg5":
+        # bounded sample: the first 1M vertices of the same seeded 10M
+        # trajectory (the generator is prefix-stable), same batch size
+        import copy
+        b = copy.copy(a)
+        b.n = min(a.n, 1_000_000)
+        seed_name = name
+        a = b
+        sample = f"first {a.n} vertices of {seed_name}; "
+    g, gm, _ = make_graph(a, 0, 1, seed_name=name)
+    dev0, dev_batches, _ = legs(a)
+    try:
+        os.sched_setaffinity(0, {min(os.sched_getaffinity(0))})
+    except (AttributeError, OSError):
+        pass
     o = Oracle(h_root=g.h_root())
     t0 = time.perf_counter()
-    s, d_, c = g.batch(2, dev0, directed=False)
-    o.append(g.h[2:dev0], s, d_, c, flags=EDGES_UNDIRECTED)
-    o.exploit()
+    for (lo, hi) in batches(dev0, a.S):
+        s, d_, c = g.batch(lo, hi, directed=False)
+        if o.append(g.h[lo:hi], s, d_, c, flags=EDGES_UNDIRECTED) > 0:
+            o.exploit()
     t_setup = time.perf_counter() - t0
-    times = []
+    times, relax = [], []
     for i, (lo, hi) in enumerate(dev_batches):
         s, d_, c = g.batch(lo, hi, directed=False)
         t = time.perf_counter()
         nprom = o.append(g.h[lo:hi], s, d_, c, flags=EDGES_UNDIRECTED)
-        if nprom > 0:
-            o.exploit()
+        st = o.exploit() if nprom > 0 else None
         o.best_path()
         dt = time.perf_counter() - t
         if i >= a.warmup:
             times.append(dt)
+            relax.append(st.relaxations if st else 0)
     ms = 1e3 * sum(times) / len(times)
-    model, ncpu = cpu_info()
     line = {
         "impl": "reference",
         "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_name(a), "d": a.d, "n": a.n, "S": a.S, "gamma": a.gamma,
+        "config": {"workload": name, "d": a.d, "n": a.n, "S": a.S, "gamma": a.gamma,
                    "boxes": a.boxes, "parallelism": "serial oracle"},
+        "relaxations_per_step": relax,
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": 1, "kind": "oracle",
-                         "sample": f"{a.steps} timed S={a.S} steps after {a.warmup} warm-up; "
-                                   f"oracle state built by itself at n={dev0} ({t_setup:.1f}s "
-                                   f"untimed); 1 of {ncpu} cores ({model})"},
+                         "sample": f"{sample}{a.steps} timed S={a.S} steps after {a.warmup} warm-up; the "
+                                   f"oracle replayed the same BE-RRT# trajectory to n={dev0} "
+                                   f"({t_setup:.1f}s untimed); pinned to 1 of {os.cpu_count()} "
+                                   f"cores ({cpu_model()})"},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    spawn_if_needed(a)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if a.impl == "reference":
+        return main_reference(a, rank, world)
+    a = resolve(a, world)
+    if a.workload == "cfg5":
+        return main_sharded(a, rank, world)
+    if world > 1:
+        raise SystemExit("cfg3 runs on one GPU; N > 1 runs configs[4] (--workload cfg5)")
+    return main_cuda_single(a)
 
 
 if __name__ == "__main__":

@@ -108,6 +108,11 @@ typedef struct {
     int32_t barriers;        /* grid-wide barriers executed                              */
     int64_t improve_set;     /* sum over Improves of |I| (vertices examined)             */
     int64_t eval_scanned;    /* out-edge entries scanned by Evaluate for children        */
+    int64_t eval_work;       /* children actually visited (an incremental Evaluate visits
+                                only the changed subtrees; eval_visits is the count of the
+                                paper's full traversal, identical in both forms)          */
+    int32_t full_evaluations;   /* Evaluates run as the full traversal ...               */
+    int32_t inc_evaluations;    /* ... and in the incremental form  */
 } pirrt_exploit_stats;
 
 /* Fill *cfg with the defaults listed above. */

@@ -156,6 +156,11 @@ struct pirrt_ctx {
     int* odidx[2] = {nullptr, nullptr}; int64_t odidx_cap[2] = {0, 0};
     // Evaluate stamps and the B lists (entry 0 = root)
     unsigned* stamp = nullptr; int64_t stamp_cap = 0;
+    unsigned* pstamp = nullptr;                          // incremental Evaluate: dirty marks,
+    int2* ccd = nullptr;                                 // child counts + depths,
+    int* dirty = nullptr;                                // dirty list (all in the hot slab)
+    int inc_max = 8192;                                  // PIRRT_INC_MAX (0: full Evaluates only)
+    int inc_validate = 0;                                // PIRRT_INC_VALIDATE=1 (test hook)
     int* Bq[2] = {nullptr, nullptr}; int64_t Bq_cap[2] = {0, 0};
     // work-queue Evaluate items (slot 0 = root, the rest -1 between Evaluates)
     int* qv = nullptr; double* qg = nullptr; int* qdepth = nullptr; int64_t q_cap = 0;
@@ -194,15 +199,10 @@ struct pirrt_ctx {
     int shard_blocks = 0;
     unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
     double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
-    int bfs_wq = 0;                                          // PIRRT_BFS=wq: work-queue Evaluate (experimental)
-    int halves = 0;                                          // PIRRT_HALVES=k: warp-per-item levels (16 lanes
-                                                             // above k * warps); 0: block-chunked edge-parallel
     int wq_keep = 32;                                        // PIRRT_WQ_KEEP
     int wq_tail = -1;                                        // PIRRT_WQ_TAIL (-1: 16 per block)
     int wq_wide = -1;                                        // PIRRT_WQ_WIDE (-1: 10 per block, 0: off)
-    int fused_append = 1;                                    // PIRRT_APPEND=split: one kernel per step
     int wide_tasks = 131072;                                 // PIRRT_WIDE_TASKS: |I| for the wide Improve (0: off)
-    int fuse_root = 1;                                       // PIRRT_FUSE_ROOT=0: root level with its own barrier
     int kids_min = -1;                                       // PIRRT_KIDS_MIN: |B| for the children index
                                                              // (-1: 4 n / mean degree; 0: never)
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
@@ -256,8 +256,11 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     cudaStream_t s = c->stream;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t sz_g = al(8 * cap), sz_pc = al(8 * cap), sz_h = al(8 * cap);
-    const size_t sz_par = al(4 * cap), sz_st = al(4 * cap), sz_bq = al(4 * (cap + 2)), sz_b = al(cap);
-    const size_t total = sz_g + sz_pc + sz_h + sz_par + sz_st + 2 * sz_bq + sz_b;
+    // B lists: members + holes stay below 4/3 n (the incremental Evaluate
+    // runs only while holes <= length / 4), so 2 cap + 2 entries suffice
+    const size_t sz_par = al(4 * cap), sz_st = al(4 * cap), sz_bq = al(4 * (2 * cap + 2)), sz_b = al(cap);
+    const size_t sz_ccd = al(8 * cap), sz_dirty = al(4 * (cap + 64));
+    const size_t total = sz_g + sz_pc + sz_h + sz_par + 2 * sz_st + 2 * sz_bq + sz_b + sz_ccd + sz_dirty;
     char* slab = nullptr;
     if (cudaMalloc(&slab, total) != cudaSuccess) { cudaGetLastError(); return fail(PIRRT_E_NOMEM, "cudaMalloc (vertex slab) failed"); }
     char* q = slab;
@@ -266,15 +269,21 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     double* h = (double*)q; q += sz_h;
     int* parent = (int*)q; q += sz_par;
     unsigned* stamp = (unsigned*)q; q += sz_st;
+    unsigned* pstamp = (unsigned*)q; q += sz_st;
+    int2* ccd = (int2*)q; q += sz_ccd;
+    int* dirty = (int*)q; q += sz_dirty;
     int* bq0 = (int*)q; q += sz_bq;
     int* bq1 = (int*)q; q += sz_bq;
     unsigned char* b = (unsigned char*)q;
     const int64_t n = c->n;
     // stamps of fresh slots read as "never visited"; list slots beyond the
-    // live entries are -1 (work-queue invariant), slot 0 = root
+    // live entries are -1 (work-queue invariant), slot 0 = root; fresh
+    // vertices have no children
     CU(cudaMemsetAsync(stamp, 0, (size_t)cap * sizeof(unsigned), s));
-    CU(cudaMemsetAsync(bq0, 0xFF, (size_t)(cap + 2) * sizeof(int), s));
-    CU(cudaMemsetAsync(bq1, 0xFF, (size_t)(cap + 2) * sizeof(int), s));
+    CU(cudaMemsetAsync(pstamp, 0, (size_t)cap * sizeof(unsigned), s));
+    CU(cudaMemsetAsync(ccd, 0, (size_t)cap * sizeof(int2), s));
+    CU(cudaMemsetAsync(bq0, 0xFF, (size_t)(2 * cap + 2) * sizeof(int), s));
+    CU(cudaMemsetAsync(bq1, 0xFF, (size_t)(2 * cap + 2) * sizeof(int), s));
     CU(cudaMemsetAsync(bq0, 0, sizeof(int), s));
     CU(cudaMemsetAsync(bq1, 0, sizeof(int), s));
     if (c->slab) {
@@ -285,6 +294,8 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
         const int64_t keep_cur = 1 + c->Bcount;
         if (cp(g, c->g, 8 * n) || cp(pc, c->pc, 8 * n) || cp(h, c->h, 8 * n) ||
             cp(parent, c->parent, 4 * n) || cp(stamp, c->stamp, 4 * n) || cp(b, c->b, n) ||
+            cp(pstamp, c->pstamp, 4 * n) || cp(ccd, c->ccd, 8 * n) ||
+            cp(dirty, c->dirty, 4 * std::min<int64_t>(n, c->vcap)) ||
             cp(nbq[c->Bsel], c->Bq[c->Bsel], 4 * keep_cur))
             return fail(PIRRT_E_CUDA, "vertex slab copy failed");
         CU(cudaStreamSynchronize(s));
@@ -292,7 +303,8 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     }
     c->slab = slab; c->slab_bytes = total;
     c->g = g; c->pc = pc; c->h = h; c->parent = parent; c->stamp = stamp; c->b = b;
-    c->Bq[0] = bq0; c->Bq[1] = bq1; c->Bq_cap[0] = c->Bq_cap[1] = cap + 2;
+    c->pstamp = pstamp; c->ccd = ccd; c->dirty = dirty;
+    c->Bq[0] = bq0; c->Bq[1] = bq1; c->Bq_cap[0] = c->Bq_cap[1] = 2 * cap + 2;
     c->g_cap = c->pc_cap = c->h_cap = c->parent_cap = c->b_cap = c->stamp_cap = cap;
     // L2 persistence for the slab
     if (c->l2_persist) {
@@ -446,6 +458,17 @@ int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
 
 int complete_pending(pirrt_ctx* c);   // below, with the exploit
 
+// The next Evaluate must be a full one (create, set_policy, an append with
+// a given policy); list_rebuilt: the B list was rebuilt without holes
+// (create, set_policy).  Stream-ordered.
+cudaError_t set_need_full(pirrt_ctx* c, bool list_rebuilt) {
+    static const int one = 1;
+    cudaError_t e = cudaMemcpyAsync(&c->ctl->need_full, &one, sizeof(int), cudaMemcpyHostToDevice,
+                                    c->stream);
+    if (e == cudaSuccess && list_rebuilt) e = cudaMemsetAsync(&c->ctl->holes, 0, sizeof(int), c->stream);
+    return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -488,15 +511,13 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_WATCHDOG_MS"))
         c->watchdog_ns = (unsigned long long)std::strtoull(w, nullptr, 10) * 1000000ull;
     if (const char* w = std::getenv("PIRRT_COMPACT_MIN")) c->compact_min = std::atof(w);
-    if (const char* w = std::getenv("PIRRT_BFS")) c->bfs_wq = std::strcmp(w, "wq") == 0;
-    if (const char* w = std::getenv("PIRRT_HALVES")) c->halves = std::max(0, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_WQ_KEEP")) c->wq_keep = std::max(1, std::min(64, std::atoi(w)));
     if (const char* w = std::getenv("PIRRT_WQ_TAIL")) c->wq_tail = std::atoi(w);
     if (const char* w = std::getenv("PIRRT_WQ_WIDE")) c->wq_wide = std::atoi(w);
-    if (const char* w = std::getenv("PIRRT_APPEND")) c->fused_append = std::strcmp(w, "split") != 0;
     if (const char* w = std::getenv("PIRRT_WIDE_TASKS")) c->wide_tasks = std::max(0, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_KIDS_MIN")) c->kids_min = std::atoi(w);
-    if (const char* w = std::getenv("PIRRT_FUSE_ROOT")) c->fuse_root = std::atoi(w);
+    if (const char* w = std::getenv("PIRRT_INC_MAX")) c->inc_max = std::max(0, std::atoi(w));
+    if (const char* w = std::getenv("PIRRT_INC_VALIDATE")) c->inc_validate = std::atoi(w) != 0;
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -588,6 +609,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         cudaMemsetAsync(c->odoff[0], 0, 3 * sizeof(long long), s) != cudaSuccess ||
 
         cudaMemsetAsync(c->ctl, 0, sizeof(DevCtl), s) != cudaSuccess ||
+        set_need_full(c, true) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "create: init copies"));
     c->n = 2;
@@ -686,15 +708,15 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     a.undirected = undirected ? 1 : 0;
     a.validate = ((flags | c->cfg.flags) & PIRRT_F_VALIDATE) ? 1 : 0;
     a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
+    a.ccd = c->ccd;
     a.n_old = n_old; a.n_new = n_new; a.base_edges = c->base_edges;
     a.ctl = c->ctl;
     a.grid_blocks = c->num_sms;
     a.per_sm = c->append_per_sm;
     a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
     const long long l0 = g_kernel_launches;
-    cudaError_t e = c->fused_append
-        ? launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks, c->l2win, s)
-        : launch_append(a, s);
+    cudaError_t e = launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks,
+                                        c->l2win, s);
     if (e == cudaSuccess && a.validate) {
         // VALIDATE: duplicates against the stored graph and inside the batch;
         // a given policy must not close a parent cycle
@@ -718,6 +740,14 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     c->n = n_all;
     c->delta_edges += m_dir;
     c->Bcount += c->ctl_host->nprom;
+    if (a.validate) {
+        // the fused kernel leaves the child counts of a VALIDATE append (which
+        // the checks after it may still reject) to this point
+        const long long l2 = g_kernel_launches;
+        CU(launch_child_count(c->parent, n_old, n_all, c->ccd, s));
+        c->launches += g_kernel_launches - l2;
+    }
+    if (parent_new) CU(set_need_full(c, false));   // a given policy: the next Evaluate is a full one
     if (n_new_promising) *n_new_promising = c->ctl_host->nprom;
     if ((rc = compact_if_needed(c, m_dir))) { c->broken = true; return rc; }
     return PIRRT_OK;
@@ -737,6 +767,9 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.odoff = c->odoff[c->cur]; a.odidx = c->odidx[c->cur];
     a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
     a.stamp = c->stamp;
+    a.pstamp = c->pstamp; a.ccd = c->ccd; a.dirty = c->dirty;
+    a.inc_max = c->inc_max;
+    a.inc_validate = c->inc_validate;
     a.Bq0 = c->Bq[0]; a.Bq1 = c->Bq[1]; a.Bsel = c->Bsel; a.Bcount = c->Bcount;
     a.old_Bcount = 0; a.pending = 0;
     a.ev_base = c->ev_next;
@@ -746,13 +779,10 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.eps = c->cfg.epsilon;
     a.prune_off = (c->cfg.flags & PIRRT_F_PRUNE_OFF) ? 1 : 0;
     a.watchdog_ns = c->watchdog_ns;
-    a.bfs_wq = c->bfs_wq;
     a.wq_keep = c->wq_keep;
     // the hand-over frontier must fit the blocks' local frontiers (64 each)
     a.wq_tail = c->wq_tail < 0 ? 16 * c->grid_blocks : std::min(c->wq_tail, 64 * c->grid_blocks);
     a.wq_wide = c->wq_wide < 0 ? 10 * c->grid_blocks : c->wq_wide;
-    a.halves = c->halves;
-    a.fuse_root = c->fuse_root;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
     a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;
     a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
@@ -936,6 +966,9 @@ int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
         st->improve_set = h.improve_set;
         st->eval_scanned = h.eval_scanned;
         st->barriers = h.barriers;
+        st->eval_work = h.work_visits;
+        st->full_evaluations = h.full_evals;
+        st->inc_evaluations = h.inc_evals;
     }
     if (h.abort_at) {
         c->broken = true;
@@ -1147,6 +1180,13 @@ int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, con
     const long long l1 = g_kernel_launches;
     CU(launch_rebuild_blist(c->b, n, c->Bq[c->Bsel], cnt_dev, c->cnt, c->scan_tmp, s));
     c->launches += g_kernel_launches - l1;
+    // policy-tree child counts of the restored policy; the next Evaluate
+    // is a full one (the incremental form needs the last Evaluate's B)
+    CU(cudaMemsetAsync(c->ccd, 0, (size_t)n * sizeof(int2), s));
+    const long long l2 = g_kernel_launches;
+    CU(launch_child_count(c->parent, 0, n, c->ccd, s));
+    c->launches += g_kernel_launches - l2;
+    CU(set_need_full(c, true));
     int bc = 0;
     CU(cudaMemcpyAsync(&bc, cnt_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));

@@ -52,6 +52,12 @@ struct IterCtl {
     alignas(128) int qout;                     // (children created - items expanded): -F0 = done
     alignas(128) int bcnt;                     // entries written to the new B list
     alignas(128) int l1cnt;                    // fused root levels: expanded children of the root
+    // incremental Evaluate (one atomic per block each)
+    alignas(128) int removed;                  // B-list members that left B
+    int orphan;                                // a removed member had children: validate the list
+    int maxd;                                  // levels of the equivalent full Evaluate
+    long long work_visits;                     // children actually visited (the algorithmic
+                                               // count, Sum over B u {root} of children, is `visits`)
 };
 
 // One Improve result in sharded mode (all-gathered between ranks).
@@ -74,6 +80,8 @@ struct DevCtl {
     int abort_at;                 // watchdog: barrier index at which all threads stop
     double last_dg;
     long long relaxations, eval_visits, improve_set, eval_scanned;
+    long long work_visits;        // children actually visited (incremental Evaluates visit fewer)
+    int full_evals, inc_evals;    // Evaluates run in full / incremental form
     unsigned long long t_improve, t_evaluate;
     unsigned long long dbg_work_ns;   // PIRRT_DEBUG level trace
     unsigned long long dbg[8];        // PIRRT_LEVEL_TRACE work-queue counters
@@ -90,6 +98,16 @@ struct DevCtl {
     int sweeps;                   // local-relaxation sweeps
     alignas(128) int nprom;       // new promising vertices
     alignas(128) int sweep_changed[2];
+    // ---- persistent across exploits (zeroed only at create): the state
+    // the incremental Evaluate needs ("incremental
+    // Evaluate").  Written by the lead thread after an Evaluate's last grid
+    // barrier (or by the host between calls), read at the next Evaluate.
+    alignas(128) int dirty_count[2];  // Improve commits pending for Evaluate ev, slot ev & 1
+    alignas(128) int need_full;       // next Evaluate must be full (create, set_policy, given policy)
+    int n_eval;                       // |V| at the last Evaluate (ids >= n_eval: appended since)
+    int Bc_eval;                      // B-list length after the last Evaluate (later slots: appends)
+    int holes;                        // -1 slots in the current B list (removed members)
+    double thr_prev;                  // thr of the last Evaluate
 };
 
 // Everything the persistent exploit kernel touches.
@@ -113,6 +131,11 @@ struct ExploitArgs {
     double* pc;
     unsigned char* b;
     unsigned* stamp;              // 2e: visited in Evaluate e; 2e+1: expanded in e
+    unsigned* pstamp;             // e: (parent, pc) committed by an Improve since Evaluate e-1
+    int2* ccd;                    // per vertex {children in the policy tree, depth at last visit}
+    int* dirty;                   // Improve commits awaiting the next Evaluate (pstamp dedups)
+    int inc_max;                  // incremental Evaluate when its start items <= this (0: never)
+    int inc_validate;             // test hook: always run the incremental list validation
     // work-queue Evaluate: item of queue slot i (qv[i] == -1: not yet published)
     int* qv;
     double* qg;
@@ -134,8 +157,6 @@ struct ExploitArgs {
     double eps;
     int prune_off;
     unsigned long long watchdog_ns;   // abort the loop after this long (diagnostic guard)
-    int bfs_wq;                       // 1: work-queue Evaluate, 0: level-synchronous
-    int halves;                       // level-synchronous: 16 lanes per vertex above halves * warps
     int wq_keep;                      // work-queue Evaluate: items a block keeps per local level
     int wq_tail;                      // level-synchronous: hand a shrinking frontier of at most
                                       // this many items to the work queue (0: never)
@@ -154,7 +175,6 @@ struct ExploitArgs {
     int* kids;                        // [n]
     int* kids_bsum;                   // [grid blocks] scan partials
     int kids_variant;                 // launch the instantiation that can use the index
-    int fuse_root;                    // Evaluate levels 0 and 1 without a grid barrier between
 };
 
 // ---- goal set (reading R4, goal-set form) ----
@@ -233,6 +253,7 @@ struct AppendArgs {
     int validate;
     // vertex SoA (write slots >= n_old only)
     double* g; double* h; int* parent; double* pc; unsigned char* b;
+    int2* ccd;                    // child counts (parents of the new vertices gain one)
     int n_old, n_new;
     long long base_edges;
     long long obase_edges;
@@ -244,8 +265,9 @@ struct AppendArgs {
     const int* goals;             // goal set (R4); the promising threshold of the
     int n_goals;                  // new vertices is the goal cost before the batch
 };
-cudaError_t launch_append(const AppendArgs& a, cudaStream_t s);
 // one cooperative kernel for the whole append; bsum needs 2 * max_blocks entries
+// child counts ccd[p].x += 1 for every parent p of [v0, v1)
+cudaError_t launch_child_count(const int* parent, int v0, int v1, int2* ccd, cudaStream_t s);
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
                                 int max_blocks, const L2Window& w, cudaStream_t s);
 constexpr int kAppendMaxBlocks = 2048;

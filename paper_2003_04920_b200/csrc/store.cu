@@ -121,127 +121,6 @@ __global__ void k_scan_apply(const long long* in, long long L, const long long* 
 
 __global__ void k_set_ll(long long* p, long long v) { *p = v; }
 
-// ------------------------------------------------------------------ append
-// validation (R12): ids in range, no self-loop, finite non-negative cost/h
-__global__ void k_validate(const int* src, const int* dst, const double* cost, long long m,
-                           const double* h_in, const int* parent_in, const double* g_in,
-                           int n_old, int n_new, DevCtl* ctl) {
-    const long long n_all = (long long)n_old + n_new;
-    int err = 0;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        const int s = src[e], d = dst[e];
-        const double c = cost[e];
-        if (s < 0 || s >= n_all || d < 0 || d >= n_all) err |= kErrRange;
-        else if (s == d) err |= kErrSelfLoop;
-        if (!(c >= 0.0) || isinf(c)) err |= kErrCost;
-    }
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += stride) {
-        const double hv = h_in[i];
-        if (!(hv >= 0.0) || isinf(hv)) err |= kErrH;
-        if (parent_in) {
-            const int p = parent_in[i];
-            const double gv = g_in[i];
-            if (p < -1 || p >= n_all || p == n_old + i) err |= kErrRange;
-            else if (p < 0 && !isinf(gv)) err |= kErrGNew;
-            else if (p >= 0 && (!(gv >= 0.0) || isinf(gv))) err |= kErrGNew;
-        }
-    }
-    if (err) atomicOr(&ctl->err, err);
-}
-
-// cnt[v] = delta-row length of v before the append (0 for new vertices)
-__global__ void k_delta_count(const long long* doff_old, int n_old, int n_all, long long* cnt,
-                              const DevCtl* ctl) {
-    if (failed(ctl)) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n_all; v += gridDim.x * blockDim.x)
-        cnt[v] = (v < n_old) ? doff_old[v + 1] - doff_old[v] : 0;
-}
-
-// dir 0: in-edge store (row = dst, value = src, with cost);
-// dir 1: out-edge index (row = src, value = dst, no cost).
-// With `undirected` every triple also contributes the reverse edge.
-__global__ void k_edge_hist(const int* src, const int* dst, long long m, int undirected, int dir,
-                            long long* cnt, const DevCtl* ctl) {
-    if (failed(ctl)) return;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        const int row = dir ? src[e] : dst[e];
-        atomicAdd((unsigned long long*)&cnt[row], 1ull);
-        if (undirected) atomicAdd((unsigned long long*)&cnt[dir ? dst[e] : src[e]], 1ull);
-    }
-}
-
-// thread per row (delta rows are short): copy the old delta row to its new
-// position and leave the row's write cursor in cursor[v]
-__global__ void k_delta_copy_old(const long long* doff_old, const int* didx_old,
-                                 const double* dcost_old, const long long* doff_new, int* didx_new,
-                                 double* dcost_new, int n_old, int n_all, long long* cursor,
-                                 const DevCtl* ctl) {
-    if (failed(ctl)) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n_all; v += gridDim.x * blockDim.x) {
-        const long long dst0 = doff_new[v];
-        long long len = 0;
-        if (v < n_old) {
-            const long long s0 = doff_old[v];
-            len = doff_old[v + 1] - s0;
-            for (long long k = 0; k < len; ++k) {
-                didx_new[dst0 + k] = didx_old[s0 + k];
-                if (dcost_new) dcost_new[dst0 + k] = dcost_old[s0 + k];
-            }
-        }
-        cursor[v] = dst0 + len;
-    }
-}
-
-__global__ void k_delta_scatter(const int* src, const int* dst, const double* cost, long long m,
-                                int undirected, int dir, long long* cursor, int* didx_new,
-                                double* dcost_new, const DevCtl* ctl) {
-    if (failed(ctl)) return;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        const int s = src[e], d = dst[e];
-        const int row = dir ? s : d, val = dir ? d : s;
-        long long p = (long long)atomicAdd((unsigned long long*)&cursor[row], 1ull);
-        didx_new[p] = val;
-        const double c = dcost_new ? cost[e] + 0.0 : 0.0;   // -0.0 -> +0.0 (R12)
-        if (dcost_new) dcost_new[p] = c;
-        if (undirected) {
-            p = (long long)atomicAdd((unsigned long long*)&cursor[val], 1ull);
-            didx_new[p] = row;
-            if (dcost_new) dcost_new[p] = c;
-        }
-    }
-}
-
-// base rows of the new vertices are empty: boff[v] = base_edges, v in (n_old, n_all]
-__global__ void k_base_extend(long long* boff, int n_old, int n_all, long long base_edges,
-                              const DevCtl* ctl) {
-    if (failed(ctl)) return;
-    for (int v = n_old + 1 + blockIdx.x * blockDim.x + threadIdx.x; v <= n_all;
-         v += gridDim.x * blockDim.x)
-        boff[v] = base_edges;
-}
-
-__global__ void k_init_new(const double* h_in, const int* parent_in, const double* g_in, int n_old,
-                           int n_new, double* g, double* h, int* parent, double* pc,
-                           unsigned char* b, const DevCtl* ctl) {
-    if (failed(ctl)) return;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += gridDim.x * blockDim.x) {
-        const int v = n_old + i;
-        h[v] = h_in[i] + 0.0;
-        if (parent_in) {
-            parent[v] = parent_in[i];
-            g[v] = g_in[i] + 0.0;
-        } else {
-            parent[v] = -1;
-            g[v] = INFINITY;
-        }
-        pc[v] = 0.0;
-        b[v] = 0;
-    }
-}
-
 // warp per new vertex with a given parent: pc(v) = cost of the stored edge
 // (parent -> v); its absence is an error.  VALIDATE: g_new == g[p] + pc.
 __global__ void k_find_pc(const long long* boff, const int* bidx, const double* bcost,
@@ -273,103 +152,6 @@ __global__ void k_find_pc(const long long* boff, const int* bidx, const double* 
                 pc[v] = c;
                 if (validate && g[v] != g[p] + c) atomicOr(&ctl->err, kErrGNew);
             }
-        }
-    }
-}
-
-// Extend's local relaxation of the new vertices (R14):
-// g(v) = lexicographic min over stored edges (u -> v), u < v, of
-// (g(u) + c, u).  Computed by chaotic (in-place) sweeps until a full sweep
-// changes no (g, parent) pair; since u < v along every dependency the fixed
-// point is unique and equals the sequential id-order result bit for bit.
-__global__ void __launch_bounds__(kBT) k_relax_new(
-    const long long* boff, const int* bidx, const double* bcost, const long long* doff,
-    const int* didx, const double* dcost, double* g, int* parent, double* pc, int n_old,
-    int n_new, DevCtl* ctl) {
-    cg::grid_group grid = cg::this_grid();
-    if (failed(ctl)) return;   // uniform: err is final before this kernel starts
-    const int lane = threadIdx.x & 31;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-    for (int s = 0;; ++s) {
-        int* chg = &ctl->sweep_changed[s & 1];
-        if (lead) ctl->sweep_changed[(s + 1) & 1] = 0;
-        bool my_change = false;
-        for (int i = w; i < n_new; i += nw) {
-            const int v = n_old + i;
-            double best = INFINITY;
-            int arg = INT_MAX;
-            double argc = 0.0;
-            for (long long k = boff[v] + lane; k < boff[v + 1]; k += 32) {
-                const int u = bidx[k];
-                if (u >= v) continue;
-                const double c = bcost[k];
-                const double cand = *(volatile const double*)&g[u] + c;
-                if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
-            }
-            for (long long k = doff[v] + lane; k < doff[v + 1]; k += 32) {
-                const int u = didx[k];
-                if (u >= v) continue;
-                const double c = dcost[k];
-                const double cand = *(volatile const double*)&g[u] + c;
-                if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
-            }
-            double wb = best;
-            int wa = arg;
-            for (int o = 16; o; o >>= 1) {
-                const double ob = __shfl_xor_sync(kFull, wb, o);
-                const int oa = __shfl_xor_sync(kFull, wa, o);
-                if (ob < wb || (ob == wb && oa < wa)) { wb = ob; wa = oa; }
-            }
-            const unsigned m = __ballot_sync(kFull, best == wb && arg == wa);
-            const double c = __shfl_sync(kFull, argc, __ffs(m) - 1);
-            if (lane == 0) {
-                int np;
-                double ng, npc;
-                if (wb < INFINITY) { np = wa; ng = wb; npc = c; }
-                else { np = -1; ng = INFINITY; npc = 0.0; }
-                if (np != parent[v] || __double_as_longlong(ng) != __double_as_longlong(g[v])) {
-                    *(volatile double*)&g[v] = ng;
-                    parent[v] = np;
-                    pc[v] = npc;
-                    my_change = true;
-                }
-            }
-        }
-        if (my_change) atomicOr(chg, 1);
-        grid.sync();
-        const int any = *(volatile int*)chg;
-        if (lead) ctl->sweeps = s + 1;
-        if (!any) break;
-        grid.sync();   // everyone has read chg before it is reset two sweeps later
-    }
-}
-
-// b(v) = g(v) + h(v) < g(x_goal) for the new vertices;
-// promising ones are appended to the B list (invisible until the host
-// commits the new count).  Goal set (R4): the threshold is the goal cost
-// before the batch (goals among the old vertices).
-__global__ void k_new_promising(const double* g, const double* h, unsigned char* b, int n_old,
-                                int n_new, int* Blist, int Bcount, DevCtl* ctl, const int* goals,
-                                int n_goals) {
-    if (failed(ctl)) return;
-    const double thr = warp_goal_cost(g, goals, n_goals, n_old);
-    const int lane = threadIdx.x & 31;
-    for (int base = blockIdx.x * blockDim.x; base < n_new; base += gridDim.x * blockDim.x) {
-        const int i = base + threadIdx.x;
-        const int v = n_old + i;
-        const bool p = (i < n_new) && (g[v] + h[v] < thr);
-        if (i < n_new) b[v] = p ? 1 : 0;
-        const unsigned m = __ballot_sync(kFull, p);
-        if (m) {
-            const int leader = __ffs(m) - 1;
-            int pos = 0;
-            if (lane == leader) pos = atomicAdd(&ctl->nprom, __popc(m));
-            pos = __shfl_sync(kFull, pos, leader);
-            unsigned lt;
-            asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
-            if (p) Blist[1 + Bcount + pos + __popc(m & lt)] = v;
         }
     }
 }
@@ -772,7 +554,15 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         const int i = base + threadIdx.x;
         const int v = n_old + i;
         const bool p = (i < n_new) && (a.g[v] + a.h[v] < thr);
-        if (i < n_new) a.b[v] = p ? 1 : 0;
+        if (i < n_new) {
+            a.b[v] = p ? 1 : 0;
+            // the new vertex is a child of its parent in the policy tree
+            // (incremental Evaluate's child counts); VALIDATE appends may
+            // still be rejected after this kernel: the host counts those
+            // after its commit
+            const int pv = a.parent[v];
+            if (!a.validate && pv >= 0) atomicAdd(&a.ccd[pv].x, 1);
+        }
         const unsigned mm = __ballot_sync(kFull, p);
         if (mm) {
             const int leader = __ffs(mm) - 1;
@@ -838,89 +628,6 @@ cudaError_t launch_cycle_check(const int* parent, int n, int* tmp, DevCtl* ctl, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_append(const AppendArgs& a, cudaStream_t s) {
-    const int n_all = a.n_old + a.n_new;
-    const long long m = a.m;
-    cudaError_t e;
-    // 1. validation
-    {
-        long long work = m > a.n_new ? m : a.n_new;
-        ++g_kernel_launches;
-        k_validate<<<grid_for(work), kBT, 0, s>>>(a.src, a.dst, a.cost, m, a.h_in, a.parent_in,
-                                                  a.g_in, a.n_old, a.n_new, a.ctl);
-    }
-    // 2. delta merge (counting sort of the new edges by row), in-edge store
-    //    (rows by destination, with cost) and out-edge index (rows by source)
-    for (int dir = 0; dir < 2; ++dir) {
-        const long long* doff_old = dir ? a.odoff_old : a.doff_old;
-        const int* didx_old = dir ? a.odidx_old : a.didx_old;
-        const double* dcost_old = dir ? nullptr : a.dcost_old;
-        long long* doff_new = dir ? a.odoff_new : a.doff_new;
-        int* didx_new = dir ? a.odidx_new : a.didx_new;
-        double* dcost_new = dir ? nullptr : a.dcost_new;
-        ++g_kernel_launches;
-        k_delta_count<<<grid_for(n_all + 1), kBT, 0, s>>>(doff_old, a.n_old, n_all, a.cnt, a.ctl);
-        if (m > 0) {
-            ++g_kernel_launches;
-            k_edge_hist<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, m, a.undirected, dir, a.cnt, a.ctl);
-        }
-        if ((e = scan_exclusive(a.cnt, doff_new, n_all, a.scan_tmp, s)) != cudaSuccess) return e;
-        ++g_kernel_launches;
-        k_delta_copy_old<<<grid_for(n_all), kBT, 0, s>>>(
-            doff_old, didx_old, dcost_old, doff_new, didx_new, dcost_new, a.n_old, n_all, a.cnt,
-            a.ctl);
-        if (m > 0) {
-            ++g_kernel_launches;
-            k_delta_scatter<<<grid_for(m), kBT, 0, s>>>(a.src, a.dst, a.cost, m, a.undirected, dir,
-                                                        a.cnt, didx_new, dcost_new, a.ctl);
-        }
-        ++g_kernel_launches;
-        k_base_extend<<<grid_for(a.n_new + 1), kBT, 0, s>>>(dir ? a.oboff_w : a.boff_w, a.n_old,
-                                                            n_all, dir ? a.obase_edges : a.base_edges,
-                                                            a.ctl);
-    }
-    // 3. new vertex state
-    if (a.n_new > 0) {
-        ++g_kernel_launches;
-        k_init_new<<<grid_for(a.n_new), kBT, 0, s>>>(a.h_in, a.parent_in, a.g_in, a.n_old, a.n_new,
-                                                     a.g, a.h, a.parent, a.pc, a.b, a.ctl);
-        if (a.parent_in) {
-            ++g_kernel_launches;
-            k_find_pc<<<grid_for((long long)a.n_new * 32), kBT, 0, s>>>(
-                a.boff, a.bidx, a.bcost, a.doff_new, a.didx_new, a.dcost_new, a.parent, a.g, a.pc,
-                a.n_old, n_all, a.validate, a.ctl);
-        } else {
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_relax_new, kBT, 0);
-            long long want = ((long long)a.n_new * 32 + kBT - 1) / kBT;
-            long long maxb = (long long)per_sm * (a.grid_blocks > 0 ? a.grid_blocks : 148);
-            int blocks = (int)(want < maxb ? want : maxb);
-            if (blocks < 1) blocks = 1;
-            const long long* boff = a.boff;
-            const int* bidx = a.bidx;
-            const double* bcost = a.bcost;
-            const long long* doff = a.doff_new;
-            const int* didx = a.didx_new;
-            const double* dcost = a.dcost_new;
-            double* g = a.g;
-            int* parent = a.parent;
-            double* pc = a.pc;
-            int n_old = a.n_old, n_new = a.n_new;
-            DevCtl* ctl = a.ctl;
-            void* params[] = {&boff, &bidx, &bcost, &doff, &didx, &dcost, &g, &parent, &pc,
-                              &n_old, &n_new, &ctl};
-            ++g_kernel_launches;
-            if ((e = cudaLaunchCooperativeKernel((const void*)k_relax_new, dim3(blocks), dim3(kBT),
-                                                 params, 0, s)) != cudaSuccess)
-                return e;
-        }
-        ++g_kernel_launches;
-        k_new_promising<<<grid_for(a.n_new), kBT, 0, s>>>(a.g, a.h, a.b, a.n_old, a.n_new, a.Blist,
-                                                          a.Bcount, a.ctl, a.goals, a.n_goals);
-    }
-    return cudaGetLastError();
-}
-
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
                                 int max_blocks, const L2Window& w, cudaStream_t s) {
     // a.per_sm: occupancy of k_append_fused, computed once per context at
@@ -932,6 +639,22 @@ cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long*
     void* params[] = {&args, &cnt1, &bsum};
     ++g_kernel_launches;
     return launch_coop((const void*)k_append_fused, blocks, kBT, params, w, s);
+}
+
+// policy-tree child counts of the parents of [v0, v1) (incremental
+// Evaluate)
+__global__ void k_child_count(const int* parent, int v0, int v1, int2* ccd) {
+    for (int v = v0 + (int)(blockIdx.x * blockDim.x + threadIdx.x); v < v1; v += gridDim.x * blockDim.x) {
+        const int p = parent[v];
+        if (p >= 0) atomicAdd(&ccd[p].x, 1);
+    }
+}
+
+cudaError_t launch_child_count(const int* parent, int v0, int v1, int2* ccd, cudaStream_t s) {
+    if (v1 <= v0) return cudaSuccess;
+    ++g_kernel_launches;
+    k_child_count<<<grid_for(v1 - v0), kBT, 0, s>>>(parent, v0, v1, ccd);
+    return cudaGetLastError();
 }
 
 int append_blocks_per_sm() {

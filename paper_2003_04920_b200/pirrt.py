@@ -88,6 +88,9 @@ class pirrt_exploit_stats(C.Structure):
         ("barriers", C.c_int32),
         ("improve_set", C.c_int64),
         ("eval_scanned", C.c_int64),
+        ("eval_work", C.c_int64),
+        ("full_evaluations", C.c_int32),
+        ("inc_evaluations", C.c_int32),
     ]
 
 
@@ -214,6 +217,9 @@ class ExploitStats:
     barriers: int
     improve_set: int
     eval_scanned: int
+    eval_work: int
+    full_evaluations: int
+    inc_evaluations: int
 
 
 def _is_torch_cuda(a) -> bool:

@@ -108,9 +108,10 @@ def test_parent_form_with_goal_set_and_sharded_loop(P):
     dual_replay(gpu, orc, with_h(r, h), 97)
 
 
-@pytest.mark.parametrize("env", [{"PIRRT_BFS": "wq", "PIRRT_WQ_KEEP": "3"},
-                                 {"PIRRT_HALVES": "1", "PIRRT_WQ_TAIL": "0", "PIRRT_WQ_WIDE": "0"},
-                                 {"PIRRT_APPEND": "split"}])
+@pytest.mark.parametrize("env", [{"PIRRT_INC_MAX": "0", "PIRRT_WQ_KEEP": "3"},
+                                 {"PIRRT_WQ_TAIL": "0", "PIRRT_WQ_WIDE": "0"},
+                                 {"PIRRT_INC_MAX": "100000", "PIRRT_WQ_KEEP": "1"},
+                                 {"PIRRT_INC_VALIDATE": "1"}])
 def test_goal_set_parent_form_variants(P, monkeypatch, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -238,7 +239,7 @@ def test_async_exploit_wait_without_start(P):
 
 # ------------------------------------------------------------ combinations
 
-@pytest.mark.parametrize("env", [{"PIRRT_KIDS_MIN": "1"}, {"PIRRT_KIDS_MIN": "1", "PIRRT_FUSE_ROOT": "0"},
+@pytest.mark.parametrize("env", [{"PIRRT_KIDS_MIN": "1"}, {"PIRRT_KIDS_MIN": "1", "PIRRT_INC_MAX": "0"},
                                  {"PIRRT_WIDE_TASKS": "1"}])
 def test_parent_form_goal_set_with_index_and_wide_improve(P, monkeypatch, env):
     # the KIDS and parent-form instantiations together, and every Improve

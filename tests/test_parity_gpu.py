@@ -276,23 +276,21 @@ def test_sharded_loop_6d(P):
     dual_replay(gpu, orc, r, 1000)
 
 
-@pytest.mark.parametrize("bfs,keep,halves,tail,wide", [
-    ("level", None, "1", "0", "0"), ("level", None, "4", None, "0"),
-    ("level", "2", None, "100000", "0"), ("level", None, None, "0", "0"),
-    ("level", None, None, None, "5"), ("level", "3", None, "0", "40"),
-    ("wq", "1", None, None, None), ("wq", "7", None, None, None), ("wq", "64", None, None, None)])
-def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves, tail, wide):
-    # the Evaluate variants must agree with the oracle: level-synchronous
-    # (block-chunked or one warp per item, 16-lane items from small frontiers
-    # on, with or without handing the shrinking tail or a wide frontier to
-    # the work queue), and
-    # the work queue from the root (its local frontier size wq_keep decides
-    # how much goes through the global queue)
-    monkeypatch.setenv("PIRRT_BFS", bfs)
+@pytest.mark.parametrize("inc,keep,tail,wide", [
+    ("0", None, "0", "0"), ("0", "2", "100000", "0"), ("0", None, None, "5"),
+    ("0", "3", "0", "40"), (None, "1", None, None), (None, "7", None, None),
+    ("100000", "64", None, None), ("3", None, None, None)])
+def test_evaluate_variants_parity(P, monkeypatch, inc, keep, tail, wide):
+    # the Evaluate forms must agree with the oracle: full traversal
+    # (PIRRT_INC_MAX=0; level-synchronous, with or without handing the
+    # shrinking tail or a wide frontier to the work queue) and incremental
+    # (default, or every Evaluate whose start set allows it; a tiny start-set
+    # limit mixes both forms); the work queue's local frontier size wq_keep
+    # decides how much goes through the global queue
+    if inc:
+        monkeypatch.setenv("PIRRT_INC_MAX", inc)
     if keep:
         monkeypatch.setenv("PIRRT_WQ_KEEP", keep)
-    if halves:
-        monkeypatch.setenv("PIRRT_HALVES", halves)
     if tail:
         monkeypatch.setenv("PIRRT_WQ_TAIL", tail)
     if wide:
@@ -304,9 +302,11 @@ def test_evaluate_variants_parity(P, monkeypatch, bfs, keep, halves, tail, wide)
 
 
 @pytest.mark.parametrize("gb", [1, 2, 5])
-def test_work_queue_small_grids_6d(P, monkeypatch, gb):
-    # few blocks: claims run far ahead of publication, staging overflows
-    monkeypatch.setenv("PIRRT_BFS", "wq")
+@pytest.mark.parametrize("inc", ["100000", "0"])
+def test_work_queue_small_grids_6d(P, monkeypatch, gb, inc):
+    # few blocks: claims run far ahead of publication, staging overflows;
+    # the incremental Evaluate's roots overflow the local frontiers
+    monkeypatch.setenv("PIRRT_INC_MAX", inc)
     monkeypatch.setenv("PIRRT_WQ_KEEP", "3")
     r = gen.rrg(6, 8000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("wq-small", gb))
     gpu = P.Context(h_root=r.h_root(), grid_blocks=gb)
@@ -325,15 +325,6 @@ def test_level_to_work_queue_handover_6d(P, monkeypatch, gb):
     gpu = P.Context(h_root=r.h_root(), grid_blocks=gb)
     orc = Oracle(h_root=r.h_root())
     dual_replay(gpu, orc, r, 700)
-
-
-def test_split_append_path_parity(P, monkeypatch):
-    # the multi-kernel append (PIRRT_APPEND=split) must agree with the fused one
-    monkeypatch.setenv("PIRRT_APPEND", "split")
-    r = gen.rrg(4, 5000, gen.gamma_k(4), n_boxes=10, seed=gen.seed_of("split"))
-    gpu = P.Context(h_root=r.h_root())
-    orc = Oracle(h_root=r.h_root())
-    dual_replay(gpu, orc, r, 333)
 
 
 @pytest.mark.parametrize("wide", ["1", "300"])
@@ -359,7 +350,7 @@ def test_wide_improve_cold_solve_and_goal_set(P, monkeypatch):
     dual_replay(gpu, orc, r, r.n)
 
 
-@pytest.mark.parametrize("env", [{}, {"PIRRT_BFS": "wq", "PIRRT_WQ_KEEP": "3"},
+@pytest.mark.parametrize("env", [{}, {"PIRRT_INC_MAX": "0", "PIRRT_WQ_KEEP": "3"},
                                  {"PIRRT_WQ_TAIL": "0", "PIRRT_WQ_WIDE": "0"},
                                  {"PIRRT_WIDE_TASKS": "500"}])
 @pytest.mark.parametrize("flags", [0, PRUNE_OFF])
@@ -408,13 +399,12 @@ def test_children_index_wide_levels_few_blocks(P, monkeypatch, gb, flags):
     dual_replay(gpu, orc, r, r.n // 2)
 
 
-@pytest.mark.parametrize("fuse", ["0", "1"])
 @pytest.mark.parametrize("gb", [1, 3, 0])
-def test_fused_root_levels_parity(P, monkeypatch, fuse, gb):
-    # Evaluate levels 0 and 1 without a barrier (every block owns the root's
-    # children at its row positions) or with one; with 1 or 3 blocks the
-    # root's row may exceed the owned capacity (fallback to the plain level)
-    monkeypatch.setenv("PIRRT_FUSE_ROOT", fuse)
+def test_fused_root_levels_parity(P, monkeypatch, gb):
+    # full Evaluates: levels 0 and 1 without a barrier (every block owns the
+    # root's children at its row positions); with 1 or 3 blocks the root's
+    # row may exceed the owned capacity (fallback to the plain level)
+    monkeypatch.setenv("PIRRT_INC_MAX", "0")
     r = gen.rrg(6, 12000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("fuse-root", gb))
     gpu = P.Context(h_root=r.h_root(), grid_blocks=gb)
     orc = Oracle(h_root=r.h_root())

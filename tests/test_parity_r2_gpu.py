@@ -1,0 +1,157 @@
+"""GPU parity for the loop-control cases and the incremental Evaluate.
+
+* The hand-built R13 / epsilon states of tests/test_oracle_loop_pins.py
+  (their expected values are derived by hand there) through the C ABI.
+* epsilon > 0 on BE-RRT# replays (R5: the last Improve's changes are kept
+  without re-evaluation, and the next exploit starts from them -- the
+  incremental Evaluate's dirty set carries over between exploits).
+* Duplicate edges without VALIDATE (a child reached through two out-row
+  entries is visited once).
+* The incremental Evaluate against the full one and the oracle, with every
+  counter (eval_visits, max_level are the full traversal's, computed from
+  child counts and depths), and the share of Evaluates that ran incrementally.
+Run on a B200: -m gpu.
+"""
+import numpy as np
+import pytest
+
+import gen
+from oracle import EDGES_UNDIRECTED, PRUNE_OFF, Oracle
+from parity import assert_same_state, assert_same_stats, dual_replay
+from test_oracle_loop_pins import chain_oracle, eps_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2003_04920_b200 import pirrt
+    return pirrt
+
+
+def gpu_chain(P, h, edges, parent, g, b, eps=0.0):
+    ctx = P.Context(h_root=h[0], h_goal=h[1], epsilon=eps)
+    src = np.array([e[0] for e in edges], np.int32)
+    dst = np.array([e[1] for e in edges], np.int32)
+    cost = np.array([e[2] for e in edges], np.float64)
+    ctx.append(np.array(h[2:], np.float64), src, dst, cost)
+    ctx.set_policy(np.array(parent, np.int32), np.array(g, np.float64), np.array(b, np.uint8))
+    return ctx
+
+
+CASES = {
+    "r13_g": ([0.0, 0.0, 0.0], [(0, 2, 1.0), (2, 1, 1.0)], [-1, 2, 0], [0.0, 10.0, 5.0], [0, 0, 1]),
+    "r13_b": ([0.0, 0.0, 100.0, 0.0, 0.0], [(0, 2, 1.0), (2, 3, 1.0), (0, 4, 1.0), (0, 1, 10.0)],
+              [-1, 0, 0, 2, 0], [0.0, 10.0, 1.0, 5.0, 1.0], [0, 0, 0, 1, 0]),
+    "r13_stall": ([0.0, 0.0, 5.0], [(0, 2, 1.0), (2, 1, 1.0)], [-1, 2, 0], [0.0, 3.0, 1.0], [0, 0, 0]),
+    "r13_parent": ([0.0, 0.0, 100.0], [(0, 2, 1.0), (2, 1, 1.0), (0, 1, 10.0)], [-1, 0, 0],
+                   [0.0, 10.0, 1.0], [0, 0, 0]),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_r13_hand_cases(P, case):
+    h, edges, parent, g, b = CASES[case]
+    gpu = gpu_chain(P, h, edges, parent, g, b)
+    orc = chain_oracle(h, edges, parent, g, b)
+    for _ in range(2):                    # and once more from the converged state
+        assert_same_stats(gpu.exploit(), orc.exploit(), case)
+        assert_same_state(gpu, orc, case)
+
+
+@pytest.mark.parametrize("eps", [8.0, 7.99, 0.0])
+def test_epsilon_hand_case(P, eps):
+    h = [0.0, 0.0, 0.0, 0.0]
+    edges = [(0, 2, 1.0), (0, 3, 0.25), (3, 2, 0.25), (2, 1, 1.0), (0, 1, 10.0)]
+    parent, g, b = [-1, 0, 0, 0], [0.0, 10.0, 1.0, 0.25], [0, 0, 1, 1]
+    gpu = gpu_chain(P, h, edges, parent, g, b, eps=eps)
+    orc = eps_oracle(eps)
+    for _ in range(2):
+        assert_same_stats(gpu.exploit(), orc.exploit(), f"eps {eps}")
+        assert_same_state(gpu, orc)
+
+
+@pytest.mark.parametrize("d,n,S,eps,inc", [(2, 4000, 40, 1e-3, None), (2, 4000, 40, 1e-2, "0"),
+                                           (6, 12000, 500, 2e-3, None), (4, 8000, 1, 5e-3, None)])
+def test_epsilon_replay(P, monkeypatch, d, n, S, eps, inc):
+    if inc:
+        monkeypatch.setenv("PIRRT_INC_MAX", inc)
+    r = gen.rrg(d, n, gen.gamma_star(d) if d == 2 else gen.gamma_k(d), n_boxes=10,
+                seed=gen.seed_of("eps", d, S))
+    gpu = P.Context(h_root=r.h_root(), epsilon=eps)
+    orc = Oracle(h_root=r.h_root(), epsilon=eps)
+    dual_replay(gpu, orc, r, S, n_stop=min(n, 2 + 300 * S))
+
+
+@pytest.mark.parametrize("inc", [None, "0"])
+def test_duplicate_edges_without_validate(P, monkeypatch, inc):
+    # every edge staged twice (and some three times): a child is reached
+    # through several out-row entries of its parent and must be visited once
+    if inc:
+        monkeypatch.setenv("PIRRT_INC_MAX", inc)
+    r = gen.rrg(3, 3000, gen.gamma_k(3), n_boxes=8, seed=gen.seed_of("dups"))
+    gpu = P.Context(h_root=r.h_root())
+    orc = Oracle(h_root=r.h_root())
+    from paper_2003_04920_b200.berrt import batches
+    for k, (a, b) in enumerate(batches(r.n, 100)):
+        s, t, c = r.batch(a, b, directed=False)
+        rep = np.concatenate([np.arange(s.size)] * 2 + [np.arange(0, s.size, 3)])
+        args = (r.h[a:b], s[rep], t[rep], c[rep])
+        assert gpu.append(*args, flags=EDGES_UNDIRECTED) == orc.append(*args, flags=EDGES_UNDIRECTED)
+        assert_same_stats(gpu.exploit(), orc.exploit(), f"batch {k}")
+        assert_same_state(gpu, orc, f"batch {k}")
+
+
+@pytest.mark.parametrize("d,n,S,gamma,flags", [(6, 20000, 256, "k", 0), (2, 8000, 1, "star", 0),
+                                               (7, 10000, 1000, "k", 0), (3, 6000, 60, "k", PRUNE_OFF)])
+def test_incremental_evaluate_is_used_and_exact(P, d, n, S, gamma, flags):
+    """Default settings: most per-batch Evaluates run incrementally; results
+    and every counter equal the oracle's (dual_replay), and eval_work (the
+    visits actually made) is below eval_visits (the full traversal's)."""
+    gm = gen.gamma_k(d) if gamma == "k" else gen.gamma_star(d)
+    r = gen.rrg(d, n, gm, n_boxes=10, seed=gen.seed_of("inc", d, S))
+    gpu = P.Context(h_root=r.h_root(), flags=flags)
+    orc = Oracle(h_root=r.h_root(), flags=flags)
+    stats = []
+
+    class Spy:
+        def __getattr__(self, k):
+            return getattr(gpu, k)
+
+        def exploit(self):
+            st = gpu.exploit()
+            stats.append(st)
+            return st
+
+    dual_replay(Spy(), orc, r, S, n_stop=min(n, 2 + 400 * S))
+    inc = sum(s.inc_evaluations for s in stats)
+    full = sum(s.full_evaluations for s in stats)
+    assert inc + full == sum(s.evaluations for s in stats)
+    assert inc > full, (inc, full)
+    assert sum(s.eval_work for s in stats) < sum(s.eval_visits for s in stats)
+
+
+def test_incremental_after_set_policy_and_given_policy(P):
+    """set_policy and an append with a given policy force the next Evaluate
+    to be full; the following ones may be incremental again."""
+    r = gen.rrg(4, 6000, gen.gamma_k(4), n_boxes=8, seed=gen.seed_of("inc-sp"))
+    gpu, orc = P.Context(h_root=r.h_root()), Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, 200, n_stop=3000, final=True)
+    parent, g, pc, b = orc.state()
+    gpu.set_policy(parent, g, b)
+    orc.set_policy(parent, g, b)
+    st = gpu.exploit()
+    assert_same_stats(st, orc.exploit())
+    # a batch with a given policy (the oracle's own local relaxation result)
+    from paper_2003_04920_b200.berrt import batches
+    for (a, bb) in batches(3600, 300, start=3000):
+        s, t, c = r.batch(a, bb, directed=False)
+        probe = Oracle(h_root=r.h_root())
+        probe.append(r.h[2:bb], *r.batch(2, bb, directed=False), flags=EDGES_UNDIRECTED)
+        pp, gg, _, _ = probe.state()
+        for ctx in (gpu, orc):
+            ctx.append(r.h[a:bb], s, t, c, parent_new=pp[a:bb], g_new=gg[a:bb], flags=EDGES_UNDIRECTED)
+        gs = gpu.exploit()
+        assert gs.full_evaluations >= (1 if gs.evaluations else 0)
+        assert_same_stats(gs, orc.exploit())
+        assert_same_state(gpu, orc)
