@@ -55,10 +55,19 @@ enum {
 enum {
     /* config flags */
     PIRRT_F_PRUNE_OFF = 1u,        /* I = V \ {root}, thr = +inf: classical PI (test/cold mode) */
-    PIRRT_F_VALIDATE = 2u,         /* extra checks: g_new consistency                           */
+    PIRRT_F_VALIDATE = 2u,         /* extra checks on append / set_policy: duplicate (src,dst)
+                                      pairs, in the batch or against the stored graph ->
+                                      E_INVAL; a parent cycle in a given
+                                      policy (set_policy, or parent_new) -> E_CORRUPT (S:179,
+                                      S:237); g_new == g(parent) + c consistency -> E_INVAL    */
     PIRRT_F_SHARDED = 16u,         /* use the sharded (NCCL) exploit loop even with nranks == 1 */
     PIRRT_F_PARENT_FORM = 32u,     /* Evaluate's promising test on the parent v, h(v)+g(v) < thr,
                                       as printed at PAPER.md:263 (variant of reading R2)         */
+    PIRRT_F_NEIGHBOURS = 64u,      /* "promising vertices and their neighbors are re-evaluated"
+                                      (NEXT-4 variant, reading R16): the
+                                      Improve set is I = B u N+(B u {x_init}) u G \ {x_init},
+                                      N+(X) = heads of the edges leaving X.  Not with
+                                      PIRRT_F_SHARDED / nranks > 1 (E_INVAL)                  */
     /* append flags */
     PIRRT_F_EDGES_UNDIRECTED = 4u, /* each (src,dst,cost) is stored in both directions         */
     PIRRT_F_DEVICE_PTRS = 8u       /* input arrays are device pointers (e.g. torch CUDA tensors)*/
@@ -90,6 +99,13 @@ typedef struct {
      * NULL/0 = {x_goal}.  E_RANGE: an id < 1. */
     const pirrt_vid* goals;
     int32_t n_goals;
+    /* Ids of x_init and x_goal.  The two vertices are the
+     * first created (Alg. 1 line 1) and ids are dense in
+     * creation order, so the only valid values are root = 0, goal = 1
+     * (reading R15); anything else -> E_INVAL.
+     * pirrt_config_init sets them. */
+    pirrt_vid root;
+    pirrt_vid goal;
 } pirrt_config;
 
 typedef struct {
@@ -113,6 +129,12 @@ typedef struct {
                                 paper's full traversal, identical in both forms)          */
     int32_t full_evaluations;   /* Evaluates run as the full traversal ...               */
     int32_t inc_evaluations;    /* ... and in the incremental form  */
+    int64_t relax_work;      /* relaxations actually made (an incremental Improve scans only
+                                the rows whose result can change; `relaxations` is the
+                                paper's full Improve count, identical in both forms)      */
+    int64_t improve_work;    /* vertices actually scanned (`improve_set` = sum of |I|)    */
+    int32_t inc_improves;    /* Improves run in the incremental form                     */
+    int32_t pad_;
 } pirrt_exploit_stats;
 
 /* Fill *cfg with the defaults listed above. */
@@ -143,8 +165,12 @@ int pirrt_destroy(pirrt_ctx* ctx);
  *               Alg. 3 replan guard (reading R10).
  * Errors: E_RANGE endpoint >= n + n_new or < 0; E_INVAL non-finite/negative
  * cost or h, self-loop, only one of parent_new/g_new given, missing parent
- * edge.  Duplicate (src,dst) pairs are the caller's responsibility (SPEC
- * S:128); Improve takes the cheapest of duplicates. */
+ * edge; with PIRRT_F_VALIDATE (config or call flags) also a duplicate
+ * (src,dst) pair in the batch or against the stored graph (E_INVAL, SPEC
+ * S:128), a g_new != g(parent) + c (E_INVAL) and a parent cycle in
+ * parent_new (E_CORRUPT).  Without VALIDATE duplicates are accepted and
+ * stored: Improve then takes the cheapest of them (lowest id on ties, R6) and
+ * Evaluate visits a child reached through several entries once. */
 int pirrt_graph_append_batch(pirrt_ctx* ctx, int32_t n_new, const double* h_new,
                              const pirrt_vid* parent_new, const double* g_new,
                              int64_t n_edges, const pirrt_vid* src, const pirrt_vid* dst,
@@ -177,11 +203,28 @@ int pirrt_exploit(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
 int pirrt_exploit_async(pirrt_ctx* ctx);
 int pirrt_exploit_wait(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
 
-/* Read-out (host outputs, cap >= pirrt_num_vertices or E_RANGE, nothing written). */
+/* Read-out of the vertex state the paper's GPU version keeps per vertex
+ * (the cost-to-come g, the parent pointer of the policy
+ * T(v) = (parent(v), v) of PAPER.md:208-212, and the promising flag b of
+ * B), plus pc(v) = c(parent(v), v) (reading R9).  Host
+ * outputs of n = pirrt_num_vertices elements, indexed by vertex id; parent -1
+ * and g +inf for a vertex not reached.  A pending asynchronous exploit is
+ * completed first.  E_INVAL NULL; E_RANGE cap < n (nothing written). */
 int pirrt_get_policy(const pirrt_ctx* ctx, pirrt_vid* parent_out, int64_t cap);
 int pirrt_get_costs(const pirrt_ctx* ctx, double* g_out, int64_t cap);
 int pirrt_get_promising(const pirrt_ctx* ctx, uint8_t* b_out, int64_t cap);
 int pirrt_get_parent_costs(const pirrt_ctx* ctx, double* pc_out, int64_t cap);
+
+/* Read-out of the stored graph (the CSR the Improve kernel reads, PAPER.md:
+ * 296-307, 351-369), rows by destination: the in-edges (u -> v, c(u, v)) of
+ * vertex v are src_out[off_out[v] .. off_out[v + 1]) with their costs in
+ * cost_out, in storage order (unspecified; Improve's result does not depend
+ * on it, R6).  off_out has n + 1 entries (cap_v >= n + 1), src_out/cost_out
+ * pirrt_num_edges entries (cap_e).  For tests and diagnostics (a full copy of
+ * the store; not for the per-batch path).  E_INVAL NULL; E_RANGE a capacity
+ * too small (nothing written). */
+int pirrt_get_in_edges(const pirrt_ctx* ctx, int64_t* off_out, int64_t cap_v, pirrt_vid* src_out,
+                       double* cost_out, int64_t cap_e);
 
 /* Policy-tree extraction (Alg. 1 lines 8-12): the branch
  * root..goal of the best goal (lowest g over the goal set, lowest id on ties;

@@ -20,6 +20,7 @@ PRUNE_OFF = 1
 VALIDATE = 2
 EDGES_UNDIRECTED = 4
 PARENT_FORM = 8
+NEIGHBOURS = 16
 
 
 class OracleError(RuntimeError):

@@ -275,7 +275,8 @@ extern "C" int orc_append(orc_ctx* c, int32_t n_new, const double* h_new,
 }
 
 // Improve (Alg. 2).  Jacobi: g is read-only here
-// (P:277-278).  I = B u {x_goal} \ {x_init} (R4); PRUNE_OFF: I = V \ {x_init}.
+// (P:277-278).  I = B u {x_goal} \ {x_init} (R4); PRUNE_OFF: I = V \ {x_init};
+// NEIGHBOURS (R16): I also holds every v with an in-edge from B u {x_init}.
 // For each v in I, the min over in-edges of c(n,v) + g(n) with lowest-id tie
 // break (R6); the policy changes only on a strict improvement over g(v)
 // (P:246).  Delta g = max over I of g(v) - g_hat (R1).
@@ -283,12 +284,23 @@ static void improve(orc_ctx* c, double* dg_out, int32_t* changed_out,
                     int64_t* relax_out) {
     const int64_t n = (int64_t)c->g.size();
     const bool prune_off = (c->flags & ORC_F_PRUNE_OFF) != 0;
+    // R16 (NEIGHBOURS variant): v also joins I when one of its
+    // in-edges (u -> v) leaves a promising vertex or the root, i.e. when v is
+    // a graph neighbour that could take a member of B u {root} as parent.
+    // Membership is fixed before any change (b is not written by Improve).
+    std::vector<uint8_t> nbr;
+    if ((c->flags & ORC_F_NEIGHBOURS) && !prune_off) {
+        nbr.assign(n, 0);
+        for (int64_t v = 0; v < n; ++v)
+            for (auto& uc : c->in[v])
+                if (uc.first == kRoot || c->b[uc.first]) { nbr[v] = 1; break; }
+    }
     double dg = 0.0;
     int32_t changed = 0;
     int64_t relax = 0;
     for (int64_t v = 0; v < n; ++v) {
         if (v == kRoot) continue;
-        if (!(prune_off || c->b[v] || is_goal(c, v))) continue;
+        if (!(prune_off || c->b[v] || is_goal(c, v) || (!nbr.empty() && nbr[v]))) continue;
         double best = kInf;
         int32_t arg = -1;
         double argc = 0.0;

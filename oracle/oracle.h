@@ -32,6 +32,9 @@ typedef struct orc_ctx orc_ctx;
 #define ORC_F_EDGES_UNDIRECTED 4u /* append: each (src,dst,cost) stored both ways */
 #define ORC_F_PARENT_FORM 8u      /* Evaluate tests the parent, h(v)+g(v) < thr, as
                                      printed at PAPER.md:263 (NEXT-4 variant of R2) */
+#define ORC_F_NEIGHBOURS 16u      /* "promising vertices and their neighbors are
+                                     re-evaluated" (NEXT-4, reading
+                                     R16): I = B u N+(B u {root}) u G \ {root}       */
 
 typedef struct {
     int32_t iterations;     /* number of Improve calls (Alg. 2)            */

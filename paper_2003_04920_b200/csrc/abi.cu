@@ -158,7 +158,16 @@ struct pirrt_ctx {
     unsigned* stamp = nullptr; int64_t stamp_cap = 0;
     unsigned* pstamp = nullptr;                          // incremental Evaluate: dirty marks,
     int2* ccd = nullptr;                                 // child counts + depths,
-    int* dirty = nullptr;                                // dirty list (all in the hot slab)
+    int* dirty = nullptr;                                // dirty lists (all in the hot slab),
+    unsigned* istamp = nullptr;                          // incremental Improve: task stamps,
+    int* gcl = nullptr;                                  // g-changed lists,
+    int* alist = nullptr;                                // task list
+    int64_t dcap = 0;                                    // entries per dirty / g-changed buffer
+    int inc_imp = 1;                                     // PIRRT_INC_IMPROVE (0 off, 1 auto, 2 always)
+    int small_grid = 0;                                  // PIRRT_SMALL_GRID: blocks for small exploits (0 off)
+    int64_t small_max = 4096;                            // PIRRT_SMALL_MAX: |B| + appended vertices bound
+    int64_t n_last_exploit = 0;                          // |V| at the last exploit's launch
+    int x_blocks = 0;                                    // grid of the running exploit
     int inc_max = 8192;                                  // PIRRT_INC_MAX (0: full Evaluates only)
     int inc_validate = 0;                                // PIRRT_INC_VALIDATE=1 (test hook)
     int* Bq[2] = {nullptr, nullptr}; int64_t Bq_cap[2] = {0, 0};
@@ -259,8 +268,13 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     // B lists: members + holes stay below 4/3 n (the incremental Evaluate
     // runs only while holes <= length / 4), so 2 cap + 2 entries suffice
     const size_t sz_par = al(4 * cap), sz_st = al(4 * cap), sz_bq = al(4 * (2 * cap + 2)), sz_b = al(cap);
-    const size_t sz_ccd = al(8 * cap), sz_dirty = al(4 * (cap + 64));
-    const size_t total = sz_g + sz_pc + sz_h + sz_par + 2 * sz_st + 2 * sz_bq + sz_b + sz_ccd + sz_dirty;
+    // dirty and g-changed lists: two buffers each (by Evaluate / Improve
+    // parity), dcap = cap + 64 entries per buffer; the incremental Improve's
+    // task list: cap entries
+    const int64_t dcap = cap + 64;
+    const size_t sz_ccd = al(8 * cap), sz_dirty = al(4 * 2 * dcap), sz_al = al(4 * cap);
+    const size_t total = sz_g + sz_pc + sz_h + sz_par + 3 * sz_st + 2 * sz_bq + sz_b + sz_ccd +
+                         2 * sz_dirty + sz_al;
     char* slab = nullptr;
     if (cudaMalloc(&slab, total) != cudaSuccess) { cudaGetLastError(); return fail(PIRRT_E_NOMEM, "cudaMalloc (vertex slab) failed"); }
     char* q = slab;
@@ -270,8 +284,11 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     int* parent = (int*)q; q += sz_par;
     unsigned* stamp = (unsigned*)q; q += sz_st;
     unsigned* pstamp = (unsigned*)q; q += sz_st;
+    unsigned* istamp = (unsigned*)q; q += sz_st;
     int2* ccd = (int2*)q; q += sz_ccd;
     int* dirty = (int*)q; q += sz_dirty;
+    int* gcl = (int*)q; q += sz_dirty;
+    int* alist = (int*)q; q += sz_al;
     int* bq0 = (int*)q; q += sz_bq;
     int* bq1 = (int*)q; q += sz_bq;
     unsigned char* b = (unsigned char*)q;
@@ -281,6 +298,7 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     // vertices have no children
     CU(cudaMemsetAsync(stamp, 0, (size_t)cap * sizeof(unsigned), s));
     CU(cudaMemsetAsync(pstamp, 0, (size_t)cap * sizeof(unsigned), s));
+    CU(cudaMemsetAsync(istamp, 0, (size_t)cap * sizeof(unsigned), s));
     CU(cudaMemsetAsync(ccd, 0, (size_t)cap * sizeof(int2), s));
     CU(cudaMemsetAsync(bq0, 0xFF, (size_t)(2 * cap + 2) * sizeof(int), s));
     CU(cudaMemsetAsync(bq1, 0xFF, (size_t)(2 * cap + 2) * sizeof(int), s));
@@ -294,8 +312,11 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
         const int64_t keep_cur = 1 + c->Bcount;
         if (cp(g, c->g, 8 * n) || cp(pc, c->pc, 8 * n) || cp(h, c->h, 8 * n) ||
             cp(parent, c->parent, 4 * n) || cp(stamp, c->stamp, 4 * n) || cp(b, c->b, n) ||
-            cp(pstamp, c->pstamp, 4 * n) || cp(ccd, c->ccd, 8 * n) ||
-            cp(dirty, c->dirty, 4 * std::min<int64_t>(n, c->vcap)) ||
+            cp(pstamp, c->pstamp, 4 * n) || cp(istamp, c->istamp, 4 * n) || cp(ccd, c->ccd, 8 * n) ||
+            cp(dirty, c->dirty, 4 * std::min<int64_t>(n, c->dcap)) ||
+            cp(dirty + dcap, c->dirty + c->dcap, 4 * std::min<int64_t>(n, c->dcap)) ||
+            cp(gcl, c->gcl, 4 * std::min<int64_t>(n, c->dcap)) ||
+            cp(gcl + dcap, c->gcl + c->dcap, 4 * std::min<int64_t>(n, c->dcap)) ||
             cp(nbq[c->Bsel], c->Bq[c->Bsel], 4 * keep_cur))
             return fail(PIRRT_E_CUDA, "vertex slab copy failed");
         CU(cudaStreamSynchronize(s));
@@ -304,6 +325,7 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     c->slab = slab; c->slab_bytes = total;
     c->g = g; c->pc = pc; c->h = h; c->parent = parent; c->stamp = stamp; c->b = b;
     c->pstamp = pstamp; c->ccd = ccd; c->dirty = dirty;
+    c->istamp = istamp; c->gcl = gcl; c->alist = alist; c->dcap = dcap;
     c->Bq[0] = bq0; c->Bq[1] = bq1; c->Bq_cap[0] = c->Bq_cap[1] = 2 * cap + 2;
     c->g_cap = c->pc_cap = c->h_cap = c->parent_cap = c->b_cap = c->stamp_cap = cap;
     // L2 persistence for the slab
@@ -465,6 +487,8 @@ cudaError_t set_need_full(pirrt_ctx* c, bool list_rebuilt) {
     static const int one = 1;
     cudaError_t e = cudaMemcpyAsync(&c->ctl->need_full, &one, sizeof(int), cudaMemcpyHostToDevice,
                                     c->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&c->ctl->imp_full, &one, sizeof(int), cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess && list_rebuilt) e = cudaMemsetAsync(&c->ctl->holes, 0, sizeof(int), c->stream);
     return e;
 }
@@ -476,6 +500,8 @@ extern "C" {
 void pirrt_config_init(pirrt_config* cfg) {
     std::memset(cfg, 0, sizeof(*cfg));
     cfg->nranks = 1;
+    cfg->root = kRoot;
+    cfg->goal = kGoal;
 }
 
 const char* pirrt_last_error(void) { return g_err.c_str(); }
@@ -492,6 +518,11 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         return fail(PIRRT_E_INVAL, "create: nranks > 1 needs nccl_unique_id");
     if (cfg.n_goals < 0 || (cfg.n_goals > 0 && !cfg.goals))
         return fail(PIRRT_E_INVAL, "create: bad goals/n_goals");
+    if ((cfg.flags & PIRRT_F_NEIGHBOURS) && (cfg.nranks > 1 || (cfg.flags & PIRRT_F_SHARDED)))
+        return fail(PIRRT_E_INVAL, "create: PIRRT_F_NEIGHBOURS is single-GPU only");
+    // R15: x_init and x_goal are the first two vertices created
+    if (cfg.root != kRoot || cfg.goal != kGoal)
+        return fail(PIRRT_E_INVAL, "create: root/goal must be 0/1 (pirrt_config_init; reading R15)");
     std::vector<int> goal_ids = {kGoal};
     for (int32_t i = 0; i < cfg.n_goals; ++i) {
         if (cfg.goals[i] < 1 || cfg.goals[i] >= kMaxVertices)
@@ -518,6 +549,9 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_KIDS_MIN")) c->kids_min = std::atoi(w);
     if (const char* w = std::getenv("PIRRT_INC_MAX")) c->inc_max = std::max(0, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_INC_VALIDATE")) c->inc_validate = std::atoi(w) != 0;
+    if (const char* w = std::getenv("PIRRT_INC_IMPROVE")) c->inc_imp = std::max(0, std::atoi(w));
+    if (const char* w = std::getenv("PIRRT_SMALL_GRID")) c->small_grid = std::max(0, std::atoi(w));
+    if (const char* w = std::getenv("PIRRT_SMALL_MAX")) c->small_max = std::max(0, std::atoi(w));
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
         c->stream = (cudaStream_t)cfg.stream;
@@ -759,7 +793,7 @@ static int kids_variant(const ExploitArgs& a, int Bcount) {
     return a.kids_min > 0 && (a.prune_off || (int64_t)Bcount + a.n_goals >= a.kids_min) ? 1 : 0;
 }
 
-static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
+static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a, int blocks) {
     std::memset(&a, 0, sizeof(a));
     a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
     a.doff = c->doff[c->cur]; a.didx = c->didx[c->cur]; a.dcost = c->dcost[c->cur];
@@ -768,7 +802,9 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
     a.stamp = c->stamp;
     a.pstamp = c->pstamp; a.ccd = c->ccd; a.dirty = c->dirty;
-    a.inc_max = c->inc_max;
+    a.istamp = c->istamp; a.gcl = c->gcl; a.alist = c->alist; a.dcap = (int)c->dcap;
+    a.inc_max = (int)std::min<int64_t>(c->inc_max, c->dcap - 64);
+    a.inc_imp = c->inc_imp;
     a.inc_validate = c->inc_validate;
     a.Bq0 = c->Bq[0]; a.Bq1 = c->Bq[1]; a.Bsel = c->Bsel; a.Bcount = c->Bcount;
     a.old_Bcount = 0; a.pending = 0;
@@ -781,12 +817,13 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a) {
     a.watchdog_ns = c->watchdog_ns;
     a.wq_keep = c->wq_keep;
     // the hand-over frontier must fit the blocks' local frontiers (64 each)
-    a.wq_tail = c->wq_tail < 0 ? 16 * c->grid_blocks : std::min(c->wq_tail, 64 * c->grid_blocks);
-    a.wq_wide = c->wq_wide < 0 ? 10 * c->grid_blocks : c->wq_wide;
+    a.wq_tail = c->wq_tail < 0 ? 16 * blocks : std::min(c->wq_tail, 64 * blocks);
+    a.wq_wide = c->wq_wide < 0 ? 10 * blocks : c->wq_wide;
     a.debug = std::getenv("PIRRT_DEBUG") != nullptr;
     a.qv = c->qv; a.qg = c->qg; a.qdepth = c->qdepth;
     a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
     a.parent_form = (c->cfg.flags & PIRRT_F_PARENT_FORM) ? 1 : 0;
+    a.neighbours = (c->cfg.flags & PIRRT_F_NEIGHBOURS) && !a.prune_off ? 1 : 0;
     // children index for large Evaluates: worth it once |B| x mean out-degree
     // exceeds ~4 n row entries; built in the append scratch (idle during an
     // exploit): cnt holds 4 (vcap + 1) ints, app_bsum >= kMaxGridBlocks ints
@@ -810,7 +847,7 @@ static int exploit_sharded(pirrt_ctx* c) {
     NcclApi* api = nccl_api();
     int rc;
     ExploitArgs a;
-    fill_exploit_args(c, a);
+    fill_exploit_args(c, a, c->shard_blocks);
     a.shard_rank = c->rank;
     a.shard_n = c->nranks;
     const long long cap = c->cfg.max_iterations > 0 ? c->cfg.max_iterations : 10LL * c->n;
@@ -889,11 +926,18 @@ int exploit_launch(pirrt_ctx* c) {
         CU(cudaEventRecord(c->ev1, s));
         return 0;
     }
-    fill_exploit_args(c, c->x_args);
+    // size-adaptive grid: a small improve set and
+    // few appended vertices since the last exploit -> a small persistent
+    // grid (cheaper grid barriers; the phases have little parallel work)
+    c->x_blocks = c->grid_blocks;
+    if (c->small_grid > 0 && (int64_t)c->Bcount + (c->n - c->n_last_exploit) <= c->small_max)
+        c->x_blocks = std::min(c->small_grid, c->grid_blocks);
+    c->n_last_exploit = c->n;
+    fill_exploit_args(c, c->x_args, c->x_blocks);
     c->x_args.wide_tasks = c->wide_tasks;
     c->x_args.it_base = 1;
     const long long l0 = g_kernel_launches;
-    cudaError_t e = launch_exploit(c->x_args, c->grid_blocks, c->l2win, s);
+    cudaError_t e = launch_exploit(c->x_args, c->x_blocks, c->l2win, s);
     c->launches += g_kernel_launches - l0;
     if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
     CU(cudaEventRecord(c->ev1, s));                      // re-recorded after every resume
@@ -931,7 +975,7 @@ int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
                 r.pending = 0;
                 r.it_base = it;
                 r.resume = 1;
-                e = launch_exploit(r, c->grid_blocks, c->l2win, s);
+                e = launch_exploit(r, c->x_blocks, c->l2win, s);
             }
             if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("exploit launch: ") + cudaGetErrorString(e)); }
             CU(cudaEventRecord(c->ev1, s));
@@ -957,7 +1001,7 @@ int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
         st->max_level = h.max_level;
         st->promising = h.promising;
         st->stalled = h.stalled;
-        st->grid_blocks = c->sharded ? c->shard_blocks : c->grid_blocks;
+        st->grid_blocks = c->sharded ? c->shard_blocks : c->x_blocks;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
         st->device_ms = ms;
@@ -969,6 +1013,9 @@ int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
         st->eval_work = h.work_visits;
         st->full_evaluations = h.full_evals;
         st->inc_evaluations = h.inc_evals;
+        st->relax_work = h.relax_work;
+        st->improve_work = h.improve_work;
+        st->inc_improves = h.inc_imps;
     }
     if (h.abort_at) {
         c->broken = true;
@@ -1073,6 +1120,42 @@ int pirrt_get_promising(const pirrt_ctx* c, uint8_t* out, int64_t cap) {
 }
 int pirrt_get_parent_costs(const pirrt_ctx* c, double* out, int64_t cap) {
     return get_array(c, out, c ? c->pc : nullptr, sizeof(double), cap, "get_parent_costs");
+}
+
+int pirrt_get_in_edges(const pirrt_ctx* cc, int64_t* off_out, int64_t cap_v, pirrt_vid* src_out,
+                       double* cost_out, int64_t cap_e) {
+    pirrt_ctx* c = const_cast<pirrt_ctx*>(cc);
+    if (!c || !off_out || !src_out || !cost_out) return fail(PIRRT_E_INVAL, "get_in_edges: NULL argument");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
+    const int64_t n = c->n, Eb = c->base_edges, Ed = c->delta_edges;
+    if (cap_v < n + 1 || cap_e < Eb + Ed) return fail(PIRRT_E_RANGE, "get_in_edges: capacity too small");
+    // base row of v, then its delta row (a copy of the store; no arithmetic)
+    std::vector<long long> bo(n + 1, 0), dq(n + 1, 0);
+    std::vector<int> bi(Eb), di(Ed);
+    std::vector<double> bc(Eb), dc(Ed);
+    cudaStream_t s = c->stream;
+    CU(cudaMemcpyAsync(bo.data(), c->boff, (n + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    if (Eb) {
+        CU(cudaMemcpyAsync(bi.data(), c->bidx, Eb * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(bc.data(), c->bcost, Eb * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    if (Ed) {
+        CU(cudaMemcpyAsync(dq.data(), c->doff[c->cur], (n + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(di.data(), c->didx[c->cur], Ed * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(dc.data(), c->dcost[c->cur], Ed * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    int64_t k = 0;
+    for (int64_t v = 0; v < n; ++v) {
+        off_out[v] = k;
+        for (long long e = bo[v]; e < bo[v + 1]; ++e, ++k) { src_out[k] = bi[e]; cost_out[k] = bc[e]; }
+        for (long long e = dq[v]; e < dq[v + 1]; ++e, ++k) { src_out[k] = di[e]; cost_out[k] = dc[e]; }
+    }
+    off_out[n] = k;
+    if (k != Eb + Ed) return fail(PIRRT_E_CORRUPT, "get_in_edges: row offsets disagree with the edge count");
+    return PIRRT_OK;
 }
 
 int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64_t* len_out,

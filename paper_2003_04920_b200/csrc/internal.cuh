@@ -58,6 +58,11 @@ struct IterCtl {
     int maxd;                                  // levels of the equivalent full Evaluate
     long long work_visits;                     // children actually visited (the algorithmic
                                                // count, Sum over B u {root} of children, is `visits`)
+    // incremental Improve: the task list's length, and the work actually
+    // done (relax / tasks are the full Improve's counts, identical in both forms)
+    alignas(128) int acount;
+    alignas(128) long long relax_work;
+    alignas(128) int tasks_work;
 };
 
 // One Improve result in sharded mode (all-gathered between ranks).
@@ -82,6 +87,8 @@ struct DevCtl {
     long long relaxations, eval_visits, improve_set, eval_scanned;
     long long work_visits;        // children actually visited (incremental Evaluates visit fewer)
     int full_evals, inc_evals;    // Evaluates run in full / incremental form
+    long long relax_work, improve_work;   // relaxations / vertices actually scanned by Improve
+    int full_imps, inc_imps;      // Improves run in full / incremental form
     unsigned long long t_improve, t_evaluate;
     unsigned long long dbg_work_ns;   // PIRRT_DEBUG level trace
     unsigned long long dbg[8];        // PIRRT_LEVEL_TRACE work-queue counters
@@ -108,6 +115,14 @@ struct DevCtl {
     int Bc_eval;                      // B-list length after the last Evaluate (later slots: appends)
     int holes;                        // -1 slots in the current B list (removed members)
     double thr_prev;                  // thr of the last Evaluate
+    // incremental Improve (same rules): gc_count[k & 1] = vertices whose g
+    // an Evaluate changed after Improve k (list gcl + (k & 1) * dcap)
+    alignas(128) int gc_count[2];
+    alignas(128) int imp_full;        // next Improve must be full (create, set_policy, full Evaluate)
+    unsigned imp_count;               // Improves so far (k of the last one)
+    int L_imp;                        // B-list length at the last Improve
+    int n_imp;                        // |V| at the last Improve
+    int c_buf, c_n;                   // its commits: dirty list c_buf, entries [0, c_n)
 };
 
 // Everything the persistent exploit kernel touches.
@@ -133,8 +148,14 @@ struct ExploitArgs {
     unsigned* stamp;              // 2e: visited in Evaluate e; 2e+1: expanded in e
     unsigned* pstamp;             // e: (parent, pc) committed by an Improve since Evaluate e-1
     int2* ccd;                    // per vertex {children in the policy tree, depth at last visit}
-    int* dirty;                   // Improve commits awaiting the next Evaluate (pstamp dedups)
+    int* dirty;                   // Improve commits awaiting Evaluate e: dirty + (e & 1) * dcap
+    int* gcl;                     // g changed by the Evaluate after Improve k: gcl + (k & 1) * dcap
+    int dcap;                     // capacity of each dirty / gcl buffer
+    unsigned* istamp;             // k: the incremental Improve k has v in its task list
+    int* alist;                   // that task list
     int inc_max;                  // incremental Evaluate when its start items <= this (0: never)
+    int inc_imp;                  // incremental Improve: 0 never, 1 when its sources are small
+                                  // next to |I| (default), 2 whenever valid (PIRRT_INC_IMPROVE)
     int inc_validate;             // test hook: always run the incremental list validation
     // work-queue Evaluate: item of queue slot i (qv[i] == -1: not yet published)
     int* qv;
@@ -166,6 +187,8 @@ struct ExploitArgs {
     const int* goals;
     int n_goals;
     int parent_form;                  // PIRRT_F_PARENT_FORM: P:263 literal test (NEXT-4)
+    int neighbours;                   // PIRRT_F_NEIGHBOURS (and not PRUNE_OFF): I = B u
+                                      // N+(B u {root}) u G (R16, NEXT-4)
     int wide_tasks;                   // hand an Improve with |I| >= this to improve_wide_kernel (0: never)
     int it_base;                      // first PI iteration of this launch (1 = a fresh exploit)
     int resume;                       // 1: iteration it_base's Improve already ran (wide kernel)

@@ -338,13 +338,20 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     // ---- P0 validation (R12)
     {
         int err = 0;
+        bool oldold = false;
         for (long long e = tid; e < m; e += nthreads) {
             const int sv = a.src[e], dv = a.dst[e];
             const double c = a.cost[e];
             if (sv < 0 || sv >= n_all || dv < 0 || dv >= n_all) err |= kErrRange;
             else if (sv == dv) err |= kErrSelfLoop;
+            else if (sv < n_old && dv < n_old) oldold = true;
             if (!(c >= 0.0) || isinf(c)) err |= kErrCost;
         }
+        // an edge between two old vertices gives an old vertex a new in-edge
+        // that the incremental Improve's sources (appended vertices and
+        // their out-neighbours) do not cover: the next Improve is a full one
+        // (set even if the batch is rejected later: only a full Improve more)
+        if (oldold) ctl->imp_full = 1;
         for (int i = tid; i < n_new; i += nthreads) {
             const double hv = a.h_in[i];
             if (!(hv >= 0.0) || isinf(hv)) err |= kErrH;

@@ -37,13 +37,14 @@ PIRRT_F_EDGES_UNDIRECTED = 4
 PIRRT_F_DEVICE_PTRS = 8
 PIRRT_F_SHARDED = 16
 PIRRT_F_PARENT_FORM = 32
+PIRRT_F_NEIGHBOURS = 64
 NCCL_UNIQUE_ID_BYTES = 128
 
 # every symbol include/pirrt.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "pirrt_config_init", "pirrt_create", "pirrt_destroy", "pirrt_graph_append_batch",
     "pirrt_exploit", "pirrt_exploit_async", "pirrt_exploit_wait", "pirrt_get_policy",
-    "pirrt_get_costs", "pirrt_get_promising", "pirrt_get_parent_costs", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
+    "pirrt_get_costs", "pirrt_get_promising", "pirrt_get_parent_costs", "pirrt_get_in_edges", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
     "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id",
     "pirrt_set_world", "pirrt_extend_batch", "pirrt_get_points",
     # include/pirrt_bench.h (measurement helpers)
@@ -68,6 +69,8 @@ class pirrt_config(C.Structure):
         ("nccl_unique_id", C.c_void_p),
         ("goals", C.c_void_p),
         ("n_goals", C.c_int32),
+        ("root", C.c_int32),
+        ("goal", C.c_int32),
     ]
 
 
@@ -91,6 +94,10 @@ class pirrt_exploit_stats(C.Structure):
         ("eval_work", C.c_int64),
         ("full_evaluations", C.c_int32),
         ("inc_evaluations", C.c_int32),
+        ("relax_work", C.c_int64),
+        ("improve_work", C.c_int64),
+        ("inc_improves", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
@@ -115,6 +122,7 @@ def _load():
     for f in ("pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
               "pirrt_get_parent_costs"):
         getattr(lib, f).argtypes = [P, P, C.c_int64]
+    lib.pirrt_get_in_edges.argtypes = [P, P, C.c_int64, P, P, C.c_int64]
     lib.pirrt_best_path.argtypes = [P, P, C.c_int64, P, P, P]
     lib.pirrt_set_policy.argtypes = [P, P, P, P]
     lib.pirrt_num_vertices.argtypes = [P]
@@ -148,6 +156,7 @@ pirrt_get_policy = _lib.pirrt_get_policy
 pirrt_get_costs = _lib.pirrt_get_costs
 pirrt_get_promising = _lib.pirrt_get_promising
 pirrt_get_parent_costs = _lib.pirrt_get_parent_costs
+pirrt_get_in_edges = _lib.pirrt_get_in_edges
 pirrt_best_path = _lib.pirrt_best_path
 pirrt_set_policy = _lib.pirrt_set_policy
 pirrt_num_vertices = _lib.pirrt_num_vertices
@@ -220,6 +229,10 @@ class ExploitStats:
     eval_work: int
     full_evaluations: int
     inc_evaluations: int
+    relax_work: int
+    improve_work: int
+    inc_improves: int
+    pad_: int
 
 
 def _is_torch_cuda(a) -> bool:
@@ -395,6 +408,17 @@ class Context:
 
     def parent_costs(self):
         return self._get(pirrt_get_parent_costs, np.float64)
+
+    def in_edges(self):
+        """The stored graph as in-edge CSR (off[n + 1], src[E], cost[E]); row
+        order as stored (pirrt_get_in_edges)."""
+        n, E = self.n, self.n_edges
+        off = np.empty(n + 1, np.int64)
+        src = np.empty(max(E, 1), np.int32)
+        cost = np.empty(max(E, 1), np.float64)
+        _check(pirrt_get_in_edges(self._h, off.ctypes.data, n + 1, src.ctypes.data,
+                                  cost.ctypes.data, E))
+        return off, src[:E], cost[:E]
 
     def state(self):
         """(parent, g, pc, b) -- same order as the oracle's state()."""

@@ -38,6 +38,27 @@ def assert_same_stats(gs, os_, where=""):
         np.float64(os_.last_delta_g).view(np.uint64), where
 
 
+def sorted_edges(src, dst, cost):
+    """(src, dst, cost bits) rows in lexicographic (dst, src, cost bits) order."""
+    src, dst = np.asarray(src, np.int64), np.asarray(dst, np.int64)
+    cb = np.asarray(cost, np.float64).view(np.uint64)
+    order = np.lexsort((cb, src, dst))
+    return src[order], dst[order], cb[order]
+
+
+def assert_same_edge_set(gpu, src, dst, cost, where=""):
+    """The library's stored in-edge store (pirrt_get_in_edges) equals the
+    directed multiset (src, dst, cost) element by element (cost bitwise)."""
+    off, gs, gc = gpu.in_edges()
+    assert off[0] == 0 and np.all(np.diff(off) >= 0), where
+    gd = np.repeat(np.arange(off.size - 1, dtype=np.int64), np.diff(off))
+    a, b = sorted_edges(gs, gd, gc), sorted_edges(src, dst, cost)
+    assert a[0].size == b[0].size, f"{where} {a[0].size} edges stored, expected {b[0].size}"
+    for name, x, y in zip(("src", "dst", "cost"), a, b):
+        bad = np.nonzero(x != y)[0][:5]
+        assert bad.size == 0, f"{where} edge {name} differs at sorted rows {bad.tolist()}"
+
+
 def dual_replay(gpu, orc, graph, S, n_stop=None, undirected=True, check_every=1, final=True):
     """Replay BE-RRT# batches (Alg. 3) into both contexts; compare after each exploit."""
     from paper_2003_04920_b200.berrt import EDGES_UNDIRECTED, batches

@@ -63,6 +63,21 @@ def test_struct_layouts_match_header(tmp_path):
     cfg = pirrt.pirrt_config()
     pirrt.pirrt_config_init(C.byref(cfg))
     assert cfg.nranks == 1 and cfg.epsilon == 0.0 and cfg.flags == 0 and cfg.n_goals == 0
+    assert cfg.root == 0 and cfg.goal == 1          # SURVEY.md 8(b) defaults
+
+
+@pytest.mark.parametrize("root,goal", [(1, 0), (0, 2), (5, 1), (-1, 1)])
+def test_root_goal_fields_validated_without_gpu(root, goal):
+    # reading R15: x_init / x_goal are the first two vertices, so
+    # only 0 / 1 are valid; checked before any CUDA call (runs on CPU)
+    from paper_2003_04920_b200 import pirrt
+    cfg = pirrt.pirrt_config()
+    pirrt.pirrt_config_init(C.byref(cfg))
+    cfg.root, cfg.goal = root, goal
+    h = C.c_void_p()
+    rc = pirrt.pirrt_create(C.byref(cfg), C.byref(h))
+    assert rc == pirrt.PIRRT_E_INVAL
+    assert b"R15" in pirrt.pirrt_last_error()
 
 
 def test_missing_library_fails_loudly(tmp_path, monkeypatch):

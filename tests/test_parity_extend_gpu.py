@@ -8,7 +8,7 @@ import pytest
 
 import gen
 from oracle import EDGES_UNDIRECTED, Oracle
-from parity import assert_same_state, assert_same_stats
+from parity import assert_same_edge_set, assert_same_state, assert_same_stats
 from paper_2003_04920_b200.berrt import batches
 
 pytestmark = pytest.mark.gpu
@@ -46,6 +46,10 @@ def test_extend_matches_generator_and_oracle(P, d, n, S, boxes, gk):
     assert_same_state(gpu, orc, "final")
     assert gpu.n_edges == 2 * r.n_pairs
     assert np.array_equal(gpu.points(), r.points)
+    # the edge set itself, element by element: every directed (u, v, c(u, v))
+    # of the generator, cost bitwise (not only the counts)
+    src, dst, cost = r.batch(2, r.n, directed=True)
+    assert_same_edge_set(gpu, src, dst, cost, "extend")
 
 
 def test_extend_device_points_and_guards(P):

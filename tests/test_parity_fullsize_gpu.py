@@ -29,7 +29,7 @@ def test_bench_workload_full_size_parity():
     import bench
     from paper_2003_04920_b200 import pirrt
     from paper_2003_04920_b200.berrt import batches
-    a = types.SimpleNamespace(d=6, n=1_000_000, S=4096, gamma="k", boxes=20, seed=0, warmup=0,
+    a = types.SimpleNamespace(workload="cfg3", d=6, n=1_000_000, S=4096, gamma="k", boxes=20, seed=0, warmup=0,
                               steps=2, graph_cache=os.environ.get("PIRRT_FULLSIZE_CACHE", ""))
     g, gm, _ = bench.make_graph(a, 0, 1)
     S = a.S

@@ -17,7 +17,7 @@ import pytest
 
 import gen
 from oracle import EDGES_UNDIRECTED, PRUNE_OFF, Oracle
-from parity import assert_same_state, assert_same_stats, dual_replay
+from parity import assert_same_edge_set, assert_same_state, assert_same_stats, dual_replay
 from test_oracle_loop_pins import chain_oracle, eps_oracle
 
 pytestmark = pytest.mark.gpu
@@ -72,9 +72,12 @@ def test_epsilon_hand_case(P, eps):
 
 
 @pytest.mark.parametrize("d,n,S,eps,inc", [(2, 4000, 40, 1e-3, None), (2, 4000, 40, 1e-2, "0"),
-                                           (6, 12000, 500, 2e-3, None), (4, 8000, 1, 5e-3, None)])
+                                           (6, 12000, 500, 2e-3, None), (4, 8000, 1, 5e-3, None),
+                                           (6, 12000, 500, 2e-3, "imp2")])
 def test_epsilon_replay(P, monkeypatch, d, n, S, eps, inc):
-    if inc:
+    if inc == "imp2":
+        monkeypatch.setenv("PIRRT_INC_IMPROVE", "2")
+    elif inc:
         monkeypatch.setenv("PIRRT_INC_MAX", inc)
     r = gen.rrg(d, n, gen.gamma_star(d) if d == 2 else gen.gamma_k(d), n_boxes=10,
                 seed=gen.seed_of("eps", d, S))
@@ -83,11 +86,13 @@ def test_epsilon_replay(P, monkeypatch, d, n, S, eps, inc):
     dual_replay(gpu, orc, r, S, n_stop=min(n, 2 + 300 * S))
 
 
-@pytest.mark.parametrize("inc", [None, "0"])
+@pytest.mark.parametrize("inc", [None, "0", "imp2"])
 def test_duplicate_edges_without_validate(P, monkeypatch, inc):
     # every edge staged twice (and some three times): a child is reached
     # through several out-row entries of its parent and must be visited once
-    if inc:
+    if inc == "imp2":
+        monkeypatch.setenv("PIRRT_INC_IMPROVE", "2")
+    elif inc:
         monkeypatch.setenv("PIRRT_INC_MAX", inc)
     r = gen.rrg(3, 3000, gen.gamma_k(3), n_boxes=8, seed=gen.seed_of("dups"))
     gpu = P.Context(h_root=r.h_root())
@@ -100,6 +105,16 @@ def test_duplicate_edges_without_validate(P, monkeypatch, inc):
         assert gpu.append(*args, flags=EDGES_UNDIRECTED) == orc.append(*args, flags=EDGES_UNDIRECTED)
         assert_same_stats(gpu.exploit(), orc.exploit(), f"batch {k}")
         assert_same_state(gpu, orc, f"batch {k}")
+    # the stored multiset keeps every duplicate
+    s, t, c = r.batch(2, r.n, directed=False)
+    rows = []
+    for a, b in batches(r.n, 100):
+        lo, hi = np.searchsorted(t, a), np.searchsorted(t, b)
+        rep = np.concatenate([np.arange(lo, hi)] * 2 + [np.arange(lo, hi)[0::3]])
+        rows.append(rep)
+    rep = np.concatenate(rows)
+    assert_same_edge_set(gpu, np.concatenate([s[rep], t[rep]]), np.concatenate([t[rep], s[rep]]),
+                         np.concatenate([c[rep], c[rep]]), "duplicates")
 
 
 @pytest.mark.parametrize("d,n,S,gamma,flags", [(6, 20000, 256, "k", 0), (2, 8000, 1, "star", 0),
@@ -129,6 +144,29 @@ def test_incremental_evaluate_is_used_and_exact(P, d, n, S, gamma, flags):
     assert inc + full == sum(s.evaluations for s in stats)
     assert inc > full, (inc, full)
     assert sum(s.eval_work for s in stats) < sum(s.eval_visits for s in stats)
+    if not flags:
+        # incremental Improves too (PRUNE_OFF always runs the full one)
+        assert sum(s.inc_improves for s in stats) > 0
+        assert sum(s.relax_work for s in stats) < sum(s.relaxations for s in stats)
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+@pytest.mark.parametrize("d,n,S,gamma,goals", [(6, 20000, 256, "k", False), (2, 8000, 1, "star", False),
+                                               (3, 8000, 100, "k", True), (7, 10000, 1000, "star", False)])
+def test_incremental_improve_modes(P, monkeypatch, mode, d, n, S, gamma, goals):
+    """PIRRT_INC_IMPROVE=0 (every Improve full) and 2 (incremental whenever
+    its certificate is valid): identical results and counters to the oracle."""
+    monkeypatch.setenv("PIRRT_INC_IMPROVE", mode)
+    gm = gen.gamma_k(d) if gamma == "k" else gen.gamma_star(d)
+    r = gen.rrg(d, n, gm, n_boxes=10, seed=gen.seed_of("inc-imp", d, S))
+    kw = {}
+    orc = Oracle(h_root=r.h_root())
+    if goals:
+        ids = (np.nonzero(r.h[2:] <= 0.15)[0] + 2).astype(np.int32)
+        kw["goals"] = ids
+        orc.set_goals(ids)
+    gpu = P.Context(h_root=r.h_root(), **kw)
+    dual_replay(gpu, orc, r, S, n_stop=min(n, 2 + 300 * S))
 
 
 def test_incremental_after_set_policy_and_given_policy(P):
@@ -155,3 +193,46 @@ def test_incremental_after_set_policy_and_given_policy(P):
         assert gs.full_evaluations >= (1 if gs.evaluations else 0)
         assert_same_stats(gs, orc.exploit())
         assert_same_state(gpu, orc)
+
+
+@pytest.mark.parametrize("d,n,S,undirected", [(6, 20000, 256, True), (3, 6000, 1, False),
+                                              (2, 30000, 4096, True)])
+def test_stored_edge_set_after_appends_and_folds(P, d, n, S, undirected):
+    """pirrt_get_in_edges after a BE-RRT# replay (many appends, delta folds):
+    the stored graph equals the generator's directed edge multiset element by
+    element (src, dst, cost bits)."""
+    r = gen.rrg(d, n, gen.gamma_k(d), n_boxes=10, seed=gen.seed_of("edges", d, S))
+    gpu = P.Context(h_root=r.h_root())
+    from paper_2003_04920_b200.berrt import batches
+    fl = EDGES_UNDIRECTED if undirected else 0
+    for a, b in batches(r.n, S):
+        gpu.append(r.h[a:b], *r.batch(a, b, directed=not undirected), flags=fl)
+    assert gpu.n_edges == 2 * r.n_pairs
+    assert_same_edge_set(gpu, *r.batch(2, r.n, directed=True), "replay")
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_edges_between_old_vertices(P, monkeypatch, mode):
+    """Appends whose edges join two old vertices (an old vertex gains an
+    in-edge without any new vertex next to it): the incremental Improve's
+    sources do not cover it, so such an append forces the next Improve to be
+    a full one.  Each batch adds its vertices with half of their edges; the
+    other half follows as a batch with no new vertex, then an exploit."""
+    monkeypatch.setenv("PIRRT_INC_IMPROVE", mode)
+    r = gen.rrg(3, 6000, gen.gamma_k(3), n_boxes=6, seed=gen.seed_of("old-old"))
+    gpu = P.Context(h_root=r.h_root())
+    orc = Oracle(h_root=r.h_root())
+    from paper_2003_04920_b200.berrt import batches
+    U = EDGES_UNDIRECTED
+    for k, (a, b) in enumerate(batches(r.n, 200)):
+        s, t, c = r.batch(a, b, directed=False)
+        cut = int(np.searchsorted(t, (a + b) // 2))
+        pg = gpu.append(r.h[a:b], s[:cut], t[:cut], c[:cut], flags=U)
+        assert pg == orc.append(r.h[a:b], s[:cut], t[:cut], c[:cut], flags=U)
+        if pg > 0:
+            assert_same_stats(gpu.exploit(), orc.exploit(), f"batch {k}")
+        z = np.zeros(0)
+        assert gpu.append(z, s[cut:], t[cut:], c[cut:], flags=U) == 0
+        orc.append(z, s[cut:], t[cut:], c[cut:], flags=U)
+        assert_same_stats(gpu.exploit(), orc.exploit(), f"batch {k} (old-old edges)")
+    assert_same_state(gpu, orc, "final")
