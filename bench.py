@@ -50,15 +50,19 @@ METRIC = "ms per converged PI exploitation + edge relaxations/s (GTEPS) vs gathe
 B_RELAX = 20.0      # Improve relaxation: idx i32 + cost f64 streamed (12 B) + g[u] gather (8 B)
 B_IVERT = 40.0      # Improve vertex: 4 row offsets (32 B) + g[v] (8 B)
 B_VISIT = 37.0      # Evaluate visit: parent 4, pc 8, g[p] 8, g write 8, h 8, b 1
-ALGO_FORMULA = "20 B x relaxations + 40 B x improve_set + 37 B x eval_work (SURVEY.md 8(d) units)"
+ALGO_FORMULA = ("20 B x relax_work + 40 B x improve_work + 37 B x eval_work (SURVEY.md 8(d) "
+                "units, counted over the work the launch does)")
 
 
 def algo_bytes(st) -> float:
     """Bytes the launch's algorithm must move: every relaxation and Improve
-    vertex it processes, every child it visits (eval_work: an incremental
-    Evaluate visits only the changed subtrees).  Out-row entries scanned to
-    find children are implementation overhead, reported apart."""
-    return st.relaxations * B_RELAX + st.improve_set * B_IVERT + st.eval_work * B_VISIT
+    vertex it processes (relax_work / improve_work: an incremental Improve
+    scans only the rows whose result can change; `relaxations` and
+    `improve_set` are the paper's full-Improve counts), every child it visits
+    (eval_work: an incremental Evaluate visits only the changed subtrees).
+    Out-row entries scanned to find children are implementation overhead,
+    reported apart."""
+    return st.relax_work * B_RELAX + st.improve_work * B_IVERT + st.eval_work * B_VISIT
 
 
 def parse():
@@ -244,8 +248,9 @@ def ncu_traffic(workload):
 
 def counters(ex):
     """Sums of the exploit stats over a list of exploits."""
-    keys = ("relaxations", "improve_set", "eval_visits", "eval_work", "eval_scanned", "iterations",
-            "evaluations", "full_evaluations", "inc_evaluations", "barriers")
+    keys = ("relaxations", "relax_work", "improve_set", "improve_work", "eval_visits", "eval_work",
+            "eval_scanned", "iterations", "evaluations", "full_evaluations", "inc_evaluations",
+            "inc_improves", "barriers")
     return {k: int(sum(getattr(s, k) for s in ex)) for k in keys}
 
 
@@ -604,6 +609,10 @@ def main_cuda_single(a):
         "gteps": round(c["relaxations"] / (total_ms * 1e-3) / 1e9, 4),
         "exploit_ms_mean": round(ex_ms / max(1, len(ex)), 4),
         "exploit_gteps": round(c["relaxations"] / (ex_ms * 1e-3) / 1e9, 4) if ex_ms else 0,
+        "exploit_gteps_work": round(c["relax_work"] / (ex_ms * 1e-3) / 1e9, 4) if ex_ms else 0,
+        "gteps_note": "gteps = the paper's Improve relaxations (sum of |in(v)| over I, every "
+                      "iteration) per second; *_work = relaxations actually made (the "
+                      "incremental Improve skips rows whose result cannot change)",
         "append_plus_readout_ms_mean": round((total_ms - ex_ms) / a.steps, 4),
         "iterations_mean": round(c["iterations"] / max(1, len(ex)), 3),
         "promising_mean": round(statistics.mean([s.promising for s in ex]), 1) if ex else 0,

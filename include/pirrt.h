@@ -68,6 +68,10 @@ enum {
                                       Improve set is I = B u N+(B u {x_init}) u G \ {x_init},
                                       N+(X) = heads of the edges leaving X.  Not with
                                       PIRRT_F_SHARDED / nranks > 1 (E_INVAL)                  */
+    PIRRT_F_LOCAL_GROUP = 128u,    /* this context is rank `rank` of an in-process group of
+                                      `nranks` contexts (no NCCL; e.g. P ranks emulated on one
+                                      GPU for parity tests): the sharded exploit runs through
+                                      pirrt_group_exploit; pirrt_exploit returns E_STATE        */
     /* append flags */
     PIRRT_F_EDGES_UNDIRECTED = 4u, /* each (src,dst,cost) is stored in both directions         */
     PIRRT_F_DEVICE_PTRS = 8u       /* input arrays are device pointers (e.g. torch CUDA tensors)*/
@@ -250,8 +254,23 @@ int64_t pirrt_num_edges(const pirrt_ctx* ctx);   /* directed edges stored */
  * its records are all-gathered with NCCL once per PI iteration, and every
  * rank runs the identical Evaluate, so results are bit-identical to one GPU.
  * Stats: relaxations / improve_set count this rank's share.
+ * Storage (nranks > 1, without PIRRT_F_VALIDATE): the in-edge rows a fold
+ * moves into the base CSR are kept only for the vertices this rank owns, so
+ * the Improve store shrinks to ~1/nranks per rank (the out-edge index,
+ * 4 B per edge, and the vertex arrays stay replicated for the Evaluate);
+ * pirrt_get_in_edges then returns this rank's rows plus the unfolded delta,
+ * and pirrt_set_policy returns E_STATE (it needs every policy edge's cost).
  * pirrt_nccl_unique_id writes the 128-byte ncclUniqueId (call on one rank). */
 int pirrt_nccl_unique_id(void* out, int64_t cap);
+
+/* The sharded exploit of an in-process group (the same
+ * kernels and loop as one process per GPU, with the record all-gather done as
+ * device copies between the contexts' buffers): ctxs[i] is rank i of n, each
+ * created with nranks = n, rank = i, PIRRT_F_LOCAL_GROUP, and fed the same
+ * appends (SPMD).  stats (nullable) receives n entries.  The contexts may
+ * share one device and one stream.  Errors as pirrt_exploit; E_STATE if the
+ * contexts do not form such a group. */
+int pirrt_group_exploit(pirrt_ctx* const* ctxs, int32_t n, pirrt_exploit_stats* stats);
 
 /* Device-side Extend: the
  * graph-growth half of a BE-RRT# batch on the GPU, so that a batch crosses

@@ -83,6 +83,7 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char* (*errorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;   // optional
 };
 
 NcclApi* nccl_api() {
@@ -90,14 +91,18 @@ NcclApi* nccl_api() {
     static bool tried = false;
     if (!tried) {
         tried = true;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        // RTLD_LOCAL: a libnccl.so.2 torch loads later (its own build) must
+        // not resolve against this one; if torch loaded one first, the same
+        // soname returns that copy
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
         if (h) {
             api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
             api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
             api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
             api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
             api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+            api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
             if (api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy &&
                 api.errorString)
                 api.h = h;
@@ -139,7 +144,11 @@ struct pirrt_ctx {
     long long* sboff = nullptr; int64_t sboff_cap = 0;
     int* sbidx = nullptr; int64_t sbidx_cap = 0;
     double* sbcost = nullptr; int64_t sbcost_cap = 0;
-    int64_t base_edges = 0;
+    int64_t base_edges = 0;       // edges in the base CSR (this rank's rows when partitioned)
+    int64_t edges_total = 0;      // directed edges appended (pirrt_num_edges)
+    // partitioned in-edge store (sharded, nranks > 1, no VALIDATE): a fold
+    // keeps only the rows of the vertices this rank's Improve owns
+    int own_n = 0, own_r = 0;
     // delta CSR, double-buffered (cur = committed)
     long long* doff[2] = {nullptr, nullptr}; int64_t doff_cap[2] = {0, 0};
     int* didx[2] = {nullptr, nullptr}; int64_t didx_cap[2] = {0, 0};
@@ -204,7 +213,7 @@ struct pirrt_ctx {
     ncclComm_t comm = nullptr;
     ShardRec* rec_local = nullptr; int64_t rec_local_cap = 0;
     ShardRec* rec_all = nullptr; int64_t rec_all_cap = 0;
-    int* rec_counts = nullptr; int64_t rec_counts_cap = 0;   // [0] local count, [1..nranks] gathered
+    cudaEvent_t xev = nullptr, xev2 = nullptr;               // in-process group exchange ordering
     int shard_blocks = 0;
     unsigned long long watchdog_ns = 60ull * 1000000000ull;   // PIRRT_WATCHDOG_MS
     double compact_min = 32768.0;                            // PIRRT_COMPACT_MIN (edges)
@@ -388,7 +397,7 @@ void free_all(pirrt_ctx* c) {
                     c->oboff, c->obidx, c->odoff[0], c->odoff[1], c->odidx[0], c->odidx[1],
                     c->qv, c->qg, c->qdepth, c->path, c->cnt, c->scan_tmp, c->ctl,
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
-                    c->rec_local, c->rec_all, c->rec_counts, c->app_bsum, c->goals,
+                    c->rec_local, c->rec_all, c->app_bsum, c->goals,
                     c->w_boxes, c->w_goal, c->pts, c->x_cell, c->x_cpts, c->x_ccnt, c->x_cstart,
                     c->x_tmp, c->x_R, c->x_h, c->x_ecnt, c->x_eoff, c->x_src, c->x_dst, c->x_cost};
     for (void* p : ptrs)
@@ -397,6 +406,8 @@ void free_all(pirrt_ctx* c) {
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->copy_done) cudaEventDestroy(c->copy_done);
+    if (c->xev) cudaEventDestroy(c->xev);
+    if (c->xev2) cudaEventDestroy(c->xev2);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (c->comm && nccl_api()) nccl_api()->commDestroy(c->comm);
@@ -429,7 +440,7 @@ int read_ctl(pirrt_ctx* c) {
 int fold(pirrt_ctx* c, long long*& boff, int64_t& boff_cap, int*& bidx, int64_t& bidx_cap,
          double*& bcost, int64_t& bcost_cap, long long*& sboff, int64_t& sboff_cap, int*& sbidx,
          int64_t& sbidx_cap, double*& sbcost, int64_t& sbcost_cap, long long* doff,
-         const int* didx, const double* dcost, int64_t E) {
+         const int* didx, const double* dcost, int64_t E, bool partition) {
     int rc;
     if ((rc = grow(sboff, sboff_cap, c->vcap + 1, 0, c->stream))) return rc;
     if ((rc = grow(sbidx, sbidx_cap, E, 0, c->stream))) return rc;
@@ -439,6 +450,8 @@ int fold(pirrt_ctx* c, long long*& boff, int64_t& boff_cap, int*& bidx, int64_t&
     a.doff = doff; a.didx = didx; a.dcost = dcost;
     a.boff_new = sboff; a.bidx_new = sbidx; a.bcost_new = bcost ? sbcost : nullptr;
     a.cnt = c->cnt; a.scan_tmp = c->scan_tmp; a.n = c->n;
+    a.own_n = partition ? c->own_n : 0;
+    a.own_r = c->own_r;
     const long long l0 = g_kernel_launches;
     CU(launch_compact(a, c->stream));
     c->launches += g_kernel_launches - l0;
@@ -460,17 +473,24 @@ int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
     int rc;
     if ((rc = fold(c, c->boff, c->boff_cap, c->bidx, c->bidx_cap, c->bcost, c->bcost_cap,
                    c->sboff, c->sboff_cap, c->sbidx, c->sbidx_cap, c->sbcost, c->sbcost_cap,
-                   c->doff[c->cur], c->didx[c->cur], c->dcost[c->cur], E)))
+                   c->doff[c->cur], c->didx[c->cur], c->dcost[c->cur], E, true)))
         return rc;
+    int64_t Eb = E;
+    if (c->own_n > 1) {                                   // this rank's rows only
+        long long e_local = 0;
+        CU(cudaMemcpyAsync(&e_local, c->boff + c->n, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        Eb = e_local;
+    }
     double* no_cost = nullptr;
     double* no_scost = nullptr;
     int64_t no_cap = 0, no_scap = 0;
     if ((rc = fold(c, c->oboff, c->oboff_cap, c->obidx, c->obidx_cap, no_cost, no_cap,
                    c->soboff, c->soboff_cap, c->sobidx, c->sobidx_cap, no_scost, no_scap,
-                   c->odoff[c->cur], c->odidx[c->cur], nullptr, E)))
+                   c->odoff[c->cur], c->odidx[c->cur], nullptr, c->obase_edges + c->delta_edges, false)))
         return rc;
-    c->base_edges = E;
-    c->obase_edges = E;
+    c->base_edges = Eb;
+    c->obase_edges += c->delta_edges;
     c->delta_edges = 0;
     // the fold belongs to this append: finish it before returning, so that
     // it is neither hidden in nor charged to the next call on the stream
@@ -514,11 +534,15 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         return fail(PIRRT_E_INVAL, "create: invalid h_root/h_goal/epsilon/max_iterations");
     if (cfg.nranks < 1 || cfg.rank < 0 || cfg.rank >= cfg.nranks)
         return fail(PIRRT_E_INVAL, "create: bad nranks/rank");
-    if (cfg.nranks > 1 && !cfg.nccl_unique_id)
-        return fail(PIRRT_E_INVAL, "create: nranks > 1 needs nccl_unique_id");
+    const bool local_group = (cfg.flags & PIRRT_F_LOCAL_GROUP) != 0;
+    if (cfg.nranks > 1 && !cfg.nccl_unique_id && !local_group)
+        return fail(PIRRT_E_INVAL, "create: nranks > 1 needs nccl_unique_id (or PIRRT_F_LOCAL_GROUP)");
+    if (local_group && cfg.nccl_unique_id)
+        return fail(PIRRT_E_INVAL, "create: PIRRT_F_LOCAL_GROUP takes no nccl_unique_id");
     if (cfg.n_goals < 0 || (cfg.n_goals > 0 && !cfg.goals))
         return fail(PIRRT_E_INVAL, "create: bad goals/n_goals");
-    if ((cfg.flags & PIRRT_F_NEIGHBOURS) && (cfg.nranks > 1 || (cfg.flags & PIRRT_F_SHARDED)))
+    if ((cfg.flags & PIRRT_F_NEIGHBOURS) &&
+        (cfg.nranks > 1 || (cfg.flags & (PIRRT_F_SHARDED | PIRRT_F_LOCAL_GROUP))))
         return fail(PIRRT_E_INVAL, "create: PIRRT_F_NEIGHBOURS is single-GPU only");
     // R15: x_init and x_goal are the first two vertices created
     if (cfg.root != kRoot || cfg.goal != kGoal)
@@ -609,23 +633,31 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
         cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "events"));
-    if (cfg.nranks > 1 || (cfg.flags & PIRRT_F_SHARDED)) {
-        NcclApi* api = nccl_api();
-        if (!api) return bail(fail(PIRRT_E_NCCL, "create: libnccl.so.2 not loadable"));
-        ncclUniqueId id;
-        if (cfg.nccl_unique_id) std::memcpy(&id, cfg.nccl_unique_id, sizeof(id));
-        else if (api->getUniqueId(&id) != ncclSuccess) return bail(fail(PIRRT_E_NCCL, "create: ncclGetUniqueId"));
-        if (api->commInitRank(&c->comm, cfg.nranks, id, cfg.rank) != ncclSuccess)
-            return bail(fail(PIRRT_E_NCCL, "create: ncclCommInitRank"));
+    if (cfg.nranks > 1 || (cfg.flags & (PIRRT_F_SHARDED | PIRRT_F_LOCAL_GROUP))) {
+        if (!local_group) {
+            NcclApi* api = nccl_api();
+            if (!api) return bail(fail(PIRRT_E_NCCL, "create: libnccl.so.2 not loadable"));
+            ncclUniqueId id;
+            if (cfg.nccl_unique_id) std::memcpy(&id, cfg.nccl_unique_id, sizeof(id));
+            else if (api->getUniqueId(&id) != ncclSuccess) return bail(fail(PIRRT_E_NCCL, "create: ncclGetUniqueId"));
+            if (api->commInitRank(&c->comm, cfg.nranks, id, cfg.rank) != ncclSuccess)
+                return bail(fail(PIRRT_E_NCCL, "create: ncclCommInitRank"));
+        }
+        if (cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->xev2, cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(PIRRT_E_CUDA, "create: events"));
         c->sharded = true;
         c->rank = cfg.rank;
         c->nranks = cfg.nranks;
+        // partitioned in-edge store (the owner holds the
+        // in-edge rows of its vertices): folds keep only the owned rows.
+        // Not with VALIDATE, whose duplicate check reads every row
+        if (cfg.nranks > 1 && !(cfg.flags & PIRRT_F_VALIDATE)) { c->own_n = cfg.nranks; c->own_r = cfg.rank; }
         int per_sm = shard_evaluate_blocks_per_sm();
         if (per_sm < 1) return bail(fail(PIRRT_E_CUDA, "create: shard kernel does not fit an SM"));
         c->shard_blocks = cfg.grid_blocks > 0 ? std::min(cfg.grid_blocks, per_sm * c->num_sms)
                                               : per_sm * c->num_sms;
         c->shard_blocks = std::min(c->shard_blocks, kMaxGridBlocks);
-        if ((rc = grow(c->rec_counts, c->rec_counts_cap, cfg.nranks + 1, 0, c->stream))) return bail(rc);
     }
     // V = {x_init, x_goal}, E = {}, B = {}
     const double g0[2] = {0.0, INFINITY};
@@ -661,7 +693,7 @@ int pirrt_destroy(pirrt_ctx* c) {
 }
 
 int64_t pirrt_num_vertices(const pirrt_ctx* c) { return c ? c->n : 0; }
-int64_t pirrt_num_edges(const pirrt_ctx* c) { return c ? c->base_edges + c->delta_edges : 0; }
+int64_t pirrt_num_edges(const pirrt_ctx* c) { return c ? c->edges_total : 0; }
 int64_t pirrt_kernel_launches(const pirrt_ctx* c) { return c ? c->launches : 0; }
 
 int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
@@ -773,6 +805,7 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     c->cur = nb;
     c->n = n_all;
     c->delta_edges += m_dir;
+    c->edges_total += m_dir;
     c->Bcount += c->ctl_host->nprom;
     if (a.validate) {
         // the fused kernel leaves the child counts of a VALIDATE append (which
@@ -827,7 +860,7 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a, int blocks) {
     // children index for large Evaluates: worth it once |B| x mean out-degree
     // exceeds ~4 n row entries; built in the append scratch (idle during an
     // exploit): cnt holds 4 (vcap + 1) ints, app_bsum >= kMaxGridBlocks ints
-    const double E = (double)(c->base_edges + c->delta_edges);
+    const double E = (double)c->edges_total;
     const double mean_deg = c->n > 0 ? std::max(1.0, E / c->n) : 1.0;
     a.kids_min = c->kids_min >= 0 ? c->kids_min
                                   : (int)std::min<double>(INT32_MAX, std::max(4096.0, 4.0 * c->n / mean_deg));
@@ -839,71 +872,153 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a, int blocks) {
 
 // Sharded exploit: per PI iteration
 //   1. Improve over the owned part of I (v mod P == rank) -> records,
-//   2. ncclAllGather of the record counts, then of the records (padded),
+//   2. exchange: every rank's block of K + 1 records (its count in slot 0)
+//      gathered into every rank's buffer -- one ncclAllGather (one process
+//      per GPU), or device copies between the contexts of an in-process
+//      group (pirrt_group_exploit: P ranks emulated on one GPU),
 //   3. every rank applies all records and runs the identical Evaluate.
 // The global Delta g is the max over the gathered records: no all-reduce.
-static int exploit_sharded(pirrt_ctx* c) {
-    cudaStream_t s = c->stream;
-    NcclApi* api = nccl_api();
-    int rc;
-    ExploitArgs a;
-    fill_exploit_args(c, a, c->shard_blocks);
-    a.shard_rank = c->rank;
-    a.shard_n = c->nranks;
-    const long long cap = c->cfg.max_iterations > 0 ? c->cfg.max_iterations : 10LL * c->n;
-    // records: at most one per owned vertex of I
-    if ((rc = grow(c->rec_local, c->rec_local_cap, c->n / c->nranks + 2, 0, s))) return rc;
-    a.rec_out = c->rec_local;
-    a.rec_count = c->rec_counts;
-    int Bsel = c->Bsel, Bc = c->Bcount, old_Bc = 0, pending = 0;
-    unsigned ev = c->ev_next;
-    std::vector<int> counts(c->nranks + 1);
-    for (int it = 1;; ++it) {
-        if ((long long)it > cap) {
-            if (pending) {   // finish the last Evaluate's bookkeeping, then report
-                a.Bsel = Bsel; a.Bcount = 0; a.old_Bcount = old_Bc; a.pending = 1; a.ev_base = ev;
-                a.shard_n = c->nranks;
-                CU(launch_shard_improve(a, it, c->shard_blocks, s));
-            }
-            c->Bsel = Bsel; c->Bcount = Bc;
-            c->ev_next = ev;
-            return fail(PIRRT_E_NOCONV, "exploit: iteration cap exceeded");
-        }
-        CU(cudaMemsetAsync(&c->ctl->it[it & 1], 0, sizeof(IterCtl), s));
-        CU(cudaMemsetAsync(c->rec_counts, 0, sizeof(int), s));
-        a.Bsel = Bsel; a.Bcount = Bc; a.old_Bcount = old_Bc; a.pending = pending; a.ev_base = ev;
-        const int64_t tasks = a.prune_off ? (int64_t)c->n - 1 : (int64_t)Bc + a.n_goals;
-        if (c->wide_tasks > 0 && tasks >= c->wide_tasks) {
-            CU(launch_improve_wide(a, it, c->num_sms, s));   // large I: full-occupancy Improve
-        } else {
-            CU(launch_shard_improve(a, it, c->shard_blocks, s));
-        }
-        c->launches += 1;
-        NC(api->allGather(c->rec_counts, c->rec_counts + 1, 1, ncclInt32, c->comm, s));
-        CU(cudaMemcpyAsync(counts.data(), c->rec_counts, sizeof(int) * (c->nranks + 1),
-                           cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        int stride = 1;
-        for (int r = 0; r < c->nranks; ++r) stride = std::max(stride, counts[1 + r]);
-        if ((rc = grow(c->rec_all, c->rec_all_cap, (int64_t)stride * c->nranks, 0, s))) return rc;
-        NC(api->allGather(c->rec_local, c->rec_all, (size_t)stride * sizeof(ShardRec), ncclChar,
-                          c->comm, s));
-        a.pending = 0;   // leave_B was done by the Improve kernel
-        a.kids_variant = kids_variant(a, Bc);
-        CU(launch_shard_evaluate(a, it, c->rec_all, c->rec_counts + 1, stride, c->nranks,
-                                 c->shard_blocks, s));
-        c->launches += 1;
-        if ((rc = read_ctl(c))) return rc;
-        const DevCtl& h = *c->ctl_host;
-        Bsel = h.Bsel_out; Bc = h.Bcount_out; old_Bc = h.old_Bcount_out; pending = h.pending_out;
-        ev = c->ev_next + (unsigned)h.evaluations;
-        if (h.abort_at) break;
-        if (h.shard_stop) break;
+// The loop state lives on the device and a kernel enqueued after the stop
+// returns at once, so the host enqueues iterations in chunks (2, 4, 8, 16)
+// and synchronises once per chunk instead of twice per iteration.  A rank
+// that emitted more than K records stops the loop everywhere before any
+// record is applied (every rank sees the same counts); the host then
+// re-gathers that iteration with a larger K and carries on.
+static int shard_exchange(std::vector<pirrt_ctx*>& cs, int K) {
+    int rc = 0;
+    (void)rc;
+    const size_t bytes = (size_t)(K + 1) * sizeof(ShardRec);
+    if (cs.size() == 1 && cs[0]->comm) {
+        pirrt_ctx* c = cs[0];
+        NC(nccl_api()->allGather(c->rec_local, c->rec_all, bytes, ncclChar, c->comm, c->stream));
+        return 0;
     }
-    c->Bsel = Bsel;
-    c->Bcount = Bc;
-    c->ev_next = ev;
+    // in-process group: rank q's block -> every rank's buffer, after q's Improve
+    for (pirrt_ctx* q : cs) CU(cudaEventRecord(q->xev, q->stream));
+    for (pirrt_ctx* c : cs)
+        for (pirrt_ctx* q : cs) {
+            if (q != c) CU(cudaStreamWaitEvent(c->stream, q->xev, 0));
+            CU(cudaMemcpyAsync((char*)c->rec_all + (size_t)q->rank * bytes, q->rec_local, bytes,
+                               cudaMemcpyDeviceToDevice, c->stream));
+        }
+    // a rank's Evaluate resets its record count: only after every copy of it
+    for (pirrt_ctx* c : cs) CU(cudaEventRecord(c->xev2, c->stream));
+    for (pirrt_ctx* q : cs)
+        for (pirrt_ctx* c : cs)
+            if (c != q) CU(cudaStreamWaitEvent(q->stream, c->xev2, 0));
     return 0;
+}
+
+static int nccl_async_check(pirrt_ctx* c) {
+    if (!c->comm) return 0;                               // (an in-process group loads no NCCL)
+    NcclApi* api = nccl_api();
+    if (!api || !api->commGetAsyncError) return 0;
+    ncclResult_t e = ncclSuccess;
+    if (api->commGetAsyncError(c->comm, &e) != ncclSuccess || e != ncclSuccess) {
+        c->broken = true;
+        return fail(PIRRT_E_NCCL, std::string("exploit: NCCL asynchronous error: ") + api->errorString(e));
+    }
+    return 0;
+}
+
+static int exploit_sharded(std::vector<pirrt_ctx*>& cs) {
+    int rc;
+    pirrt_ctx* c0 = cs[0];
+    const int P = c0->nranks;
+    const size_t G = cs.size();
+    std::vector<ExploitArgs> A(G);
+    // records per rank: at most one per owned vertex of I
+    const int64_t rec_max = (int64_t)c0->n / P + 2;
+    int K = (int)std::min<int64_t>(rec_max, std::max<int64_t>(256, 2 * ((int64_t)c0->Bcount + 1) / P + 64));
+    for (size_t i = 0; i < G; ++i) {
+        pirrt_ctx* c = cs[i];
+        ExploitArgs& a = A[i];
+        fill_exploit_args(c, a, c->shard_blocks);
+        a.shard_rank = c->rank;
+        a.shard_n = P;
+        a.shard_dev = 1;
+        a.shard_K = K;
+        a.wide_tasks = c->wide_tasks;
+        if ((rc = grow(c->rec_local, c->rec_local_cap, rec_max + 1, 0, c->stream))) return rc;
+        if ((rc = grow(c->rec_all, c->rec_all_cap, (int64_t)P * (K + 1), 0, c->stream))) return rc;
+        a.rec_count = &c->rec_local[0].v;
+        a.rec_out = c->rec_local + 1;
+        // the device-resident loop state (DevCtl was zeroed by the caller)
+        const int st4[4] = {c->Bsel, c->Bcount, 0, 0};   // Bsel_out, Bcount_out, old_Bcount_out, pending_out
+        static_assert(offsetof(DevCtl, Bcount_out) == offsetof(DevCtl, Bsel_out) + 4 &&
+                      offsetof(DevCtl, old_Bcount_out) == offsetof(DevCtl, Bsel_out) + 8 &&
+                      offsetof(DevCtl, pending_out) == offsetof(DevCtl, Bsel_out) + 12, "DevCtl layout");
+        CU(cudaMemcpyAsync(&c->ctl->Bsel_out, st4, sizeof st4, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(&c->ctl->ev_out, &c->ev_next, sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemsetAsync(c->rec_local, 0, sizeof(ShardRec), c->stream));
+        CU(cudaStreamSynchronize(c->stream));           // (host sources above are on the stack)
+    }
+    int Bc_known = c0->Bcount, stop = 0, it = 1;
+    auto evaluate_all = [&](int itv) -> int {
+        for (size_t i = 0; i < G; ++i) {
+            A[i].shard_K = K;
+            A[i].pending = 0;
+            A[i].kids_variant = kids_variant(A[i], Bc_known);
+            CU(launch_shard_evaluate(A[i], itv, cs[i]->rec_all, P, cs[i]->shard_blocks, cs[i]->stream));
+            cs[i]->launches += 1;
+        }
+        return 0;
+    };
+    for (int chunk = 2;; chunk = std::min(2 * chunk, 16)) {
+        for (int j = 0; j < chunk; ++j, ++it) {
+            for (size_t i = 0; i < G; ++i) {
+                pirrt_ctx* c = cs[i];
+                // the device picks one of the two Improve launches (|I| vs wide_tasks)
+                if (c->wide_tasks > 0) { CU(launch_improve_wide(A[i], it, c->num_sms, c->stream)); c->launches += 1; }
+                CU(launch_shard_improve(A[i], it, c->shard_blocks, c->stream));
+                c->launches += 1;
+            }
+            if ((rc = shard_exchange(cs, K))) return rc;
+            if ((rc = evaluate_all(it))) return rc;
+        }
+        stop = 0;
+        for (size_t i = 0; i < G; ++i) {
+            if ((rc = read_ctl(cs[i]))) return rc;
+            if ((rc = nccl_async_check(cs[i]))) return rc;
+            const int si = cs[i]->ctl_host->shard_stop;
+            if (i > 0 && si != stop) { cs[i]->broken = true; return fail(PIRRT_E_CORRUPT, "exploit: ranks disagree on the stop"); }
+            stop = si;
+        }
+        const DevCtl& h = *c0->ctl_host;
+        Bc_known = h.Bcount_out;
+        if (stop == 4) {                                  // a rank had more than K records
+            const int it_o = h.shard_over_it;
+            K = (int)std::min<int64_t>(rec_max, std::max<int64_t>(2LL * h.shard_over, 2LL * K));
+            for (size_t i = 0; i < G; ++i) {
+                pirrt_ctx* c = cs[i];
+                if ((rc = grow(c->rec_all, c->rec_all_cap, (int64_t)P * (K + 1), 0, c->stream))) return rc;
+                CU(cudaMemsetAsync(&c->ctl->shard_stop, 0, sizeof(int), c->stream));
+            }
+            if ((rc = shard_exchange(cs, K))) return rc;
+            if ((rc = evaluate_all(it_o))) return rc;
+            it = it_o + 1;
+            continue;
+        }
+        if (stop || h.abort_at) break;
+    }
+    if (stop == 3) {                                      // R11 cap: finish the pending leave_B
+        for (size_t i = 0; i < G; ++i) {
+            pirrt_ctx* c = cs[i];
+            if (c->ctl_host->pending_out) {
+                A[i].shard_finish = 1;
+                CU(launch_shard_improve(A[i], it, c->shard_blocks, c->stream));
+                c->launches += 1;
+                CU(cudaStreamSynchronize(c->stream));
+            }
+        }
+    }
+    for (pirrt_ctx* c : cs) {
+        const DevCtl& h = *c->ctl_host;
+        c->Bsel = h.Bsel_out;
+        c->Bcount = h.Bcount_out;
+        c->ev_next = h.ev_out;
+    }
+    return stop == 3 ? PIRRT_E_NOCONV : 0;
 }
 
 }  // extern "C"
@@ -921,7 +1036,9 @@ int exploit_launch(pirrt_ctx* c) {
     CU(cudaEventRecord(c->ev0, s));
     c->x_rc = 0;
     if (c->sharded) {
-        c->x_rc = exploit_sharded(c);
+        if (!c->comm) return fail(PIRRT_E_STATE, "exploit: an in-process group rank runs only through pirrt_group_exploit");
+        std::vector<pirrt_ctx*> cs{c};
+        c->x_rc = exploit_sharded(cs);
         if (c->x_rc != 0 && c->x_rc != PIRRT_E_NOCONV) { c->broken = true; return c->x_rc; }
         CU(cudaEventRecord(c->ev1, s));
         return 0;
@@ -1060,6 +1177,42 @@ int pirrt_exploit(pirrt_ctx* c, pirrt_exploit_stats* st) {
     if ((rc = take_kept_failure(c))) return rc;
     if ((rc = exploit_launch(c))) return rc;
     return exploit_finish(c, st);
+}
+
+int pirrt_group_exploit(pirrt_ctx* const* ctxs, int32_t n, pirrt_exploit_stats* stats) {
+    if (!ctxs || n < 1) return fail(PIRRT_E_INVAL, "group_exploit: bad arguments");
+    std::vector<pirrt_ctx*> cs(ctxs, ctxs + n);
+    for (int32_t i = 0; i < n; ++i) {
+        pirrt_ctx* c = cs[i];
+        if (!c) return fail(PIRRT_E_INVAL, "group_exploit: NULL context");
+        if (!(c->cfg.flags & PIRRT_F_LOCAL_GROUP) || c->nranks != n || c->rank != i || c->n != cs[0]->n)
+            return fail(PIRRT_E_STATE, "group_exploit: contexts must be ranks 0..n-1 of one PIRRT_F_LOCAL_GROUP "
+                                       "group with the same graph");
+        if (c->broken) return fail(PIRRT_E_STATE, "group_exploit: context unusable");
+    }
+    int rc;
+    for (pirrt_ctx* c : cs) {
+        if ((rc = set_device(c))) return rc;
+        if ((rc = complete_pending(c))) return rc;
+        c->kept = false;
+        CU(cudaMemsetAsync(c->ctl, 0, offsetof(DevCtl, err), c->stream));
+        CU(cudaEventRecord(c->ev0, c->stream));
+        c->x_rc = 0;
+    }
+    const int lrc = exploit_sharded(cs);
+    if (lrc != 0 && lrc != PIRRT_E_NOCONV) {
+        for (pirrt_ctx* c : cs) c->broken = true;
+        return lrc;
+    }
+    int out = PIRRT_OK;
+    for (int32_t i = 0; i < n; ++i) {
+        pirrt_ctx* c = cs[i];
+        c->x_rc = lrc;
+        CU(cudaEventRecord(c->ev1, c->stream));
+        const int r = exploit_finish(c, stats ? &stats[i] : nullptr);
+        if (r != PIRRT_OK && out == PIRRT_OK) out = r;
+    }
+    return out;
 }
 
 int pirrt_exploit_async(pirrt_ctx* c) {
@@ -1207,6 +1360,9 @@ int pirrt_best_path(const pirrt_ctx* cc, pirrt_vid* path_out, int64_t cap, int64
 int pirrt_set_policy(pirrt_ctx* c, const pirrt_vid* parent, const double* g, const uint8_t* b) {
     if (!c) return fail(PIRRT_E_INVAL, "set_policy: NULL context");
     if (!parent || !g) return fail(PIRRT_E_INVAL, "set_policy: NULL array");
+    if (c->own_n > 1)
+        return fail(PIRRT_E_STATE, "set_policy: the policy-edge costs of other ranks' vertices are not "
+                                   "stored on this rank (partitioned sharded store)");
     int rc;
     if ((rc = set_device(c))) return rc;
     if ((rc = complete_pending(c))) return rc;

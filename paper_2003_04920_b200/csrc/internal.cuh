@@ -80,7 +80,11 @@ struct DevCtl {
     int iterations, evaluations, max_level, promising, stalled;
     int Bsel_out, Bcount_out;     // B list after the exploit
     int old_Bcount_out, pending_out;  // pending leave_B (sharded host loop)
-    int shard_stop;               // sharded: 0 continue, 1 converged, 2 stalled/aborted
+    int shard_stop;               // sharded: 0 continue, 1 converged, 2 stalled/aborted,
+                                  // 3 iteration cap (E_NOCONV), 4 record overflow (re-gather)
+    unsigned ev_out;              // sharded: id of the next Evaluate (device-resident loop state
+                                  // with Bsel_out, Bcount_out, old_Bcount_out, pending_out)
+    int shard_over, shard_over_it;    // record overflow: largest count, iteration
     int barriers;
     int abort_at;                 // watchdog: barrier index at which all threads stop
     double last_dg;
@@ -172,6 +176,12 @@ struct ExploitArgs {
     int shard_rank, shard_n;      // sharded Improve: owned vertices v % shard_n == shard_rank
     ShardRec* rec_out;            // sharded Improve records
     int* rec_count;
+    int shard_dev;                // sharded loop: the loop state lives in DevCtl (Bsel_out,
+                                  // Bcount_out, old_Bcount_out, pending_out, ev_out) and a
+                                  // kernel of an iteration enqueued after the stop returns at once
+    int shard_K;                  // records per rank in the gathered buffer (stride K + 1:
+                                  // slot 0 of each rank's block holds its count)
+    int shard_finish;             // only finish the last Evaluate's leave_B (after E_NOCONV)
     DevCtl* ctl;
     int n;
     int max_it;
@@ -246,9 +256,8 @@ cudaError_t launch_coop(const void* fn, int blocks, int threads, void** params,
 // ---- launchers (store.cu / exploit.cu) ----
 cudaError_t launch_exploit(const ExploitArgs& a, int blocks, const L2Window& w, cudaStream_t s);
 cudaError_t launch_shard_improve(const ExploitArgs& a, int it, int blocks, cudaStream_t s);
-cudaError_t launch_shard_evaluate(const ExploitArgs& a, int it, const ShardRec* recs,
-                                  const int* counts, int stride, int nranks, int blocks,
-                                  cudaStream_t s);
+cudaError_t launch_shard_evaluate(const ExploitArgs& a, int it, const ShardRec* recs, int nranks,
+                                  int blocks, cudaStream_t s);
 int exploit_blocks_per_sm();
 // a3 Improve of iteration `it` as its own high-occupancy launch (large I)
 cudaError_t launch_improve_wide(const ExploitArgs& a, int it, int num_sms, cudaStream_t s);
@@ -303,6 +312,8 @@ struct CompactArgs {
     long long* boff_new; int* bidx_new; double* bcost_new;
     long long* cnt; long long* scan_tmp;
     int n;
+    int own_n, own_r;             // partitioned store (sharded, P > 1): keep only the rows of
+                                  // v with v % own_n == own_r (own_n = 0: every row)
 };
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s);
 

@@ -173,18 +173,25 @@ __global__ void k_b_scatter(const unsigned char* b, int n, const long long* off,
 }
 
 // ------------------------------------------------------------------ compaction
-__global__ void k_base_count(const long long* boff, const long long* doff, int n, long long* cnt) {
+__device__ __forceinline__ bool row_kept(int v, int own_n, int own_r) {
+    return own_n <= 1 || v % own_n == own_r;
+}
+
+__global__ void k_base_count(const long long* boff, const long long* doff, int n, long long* cnt,
+                             int own_n, int own_r) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        cnt[v] = (boff[v + 1] - boff[v]) + (doff[v + 1] - doff[v]);
+        cnt[v] = row_kept(v, own_n, own_r) ? (boff[v + 1] - boff[v]) + (doff[v + 1] - doff[v]) : 0;
 }
 
 __global__ void k_base_merge(const long long* boff, const int* bidx, const double* bcost,
                              const long long* doff, const int* didx, const double* dcost,
-                             const long long* boff_new, int* bidx_new, double* bcost_new, int n) {
+                             const long long* boff_new, int* bidx_new, double* bcost_new, int n,
+                             int own_n, int own_r) {
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     for (int v = w; v < n; v += nw) {
+        if (!row_kept(v, own_n, own_r)) continue;         // (warp-uniform)
         long long o = boff_new[v];
         const long long b0 = boff[v], bl = boff[v + 1] - b0;
         for (long long k = lane; k < bl; k += 32) {
@@ -673,11 +680,12 @@ int append_blocks_per_sm() {
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
     cudaError_t e;
     ++g_kernel_launches;
-    k_base_count<<<grid_for(a.n), kBT, 0, s>>>(a.boff, a.doff, a.n, a.cnt);
+    k_base_count<<<grid_for(a.n), kBT, 0, s>>>(a.boff, a.doff, a.n, a.cnt, a.own_n, a.own_r);
     if ((e = scan_exclusive(a.cnt, a.boff_new, a.n, a.scan_tmp, s)) != cudaSuccess) return e;
     ++g_kernel_launches;
     k_base_merge<<<grid_for((long long)a.n * 32), kBT, 0, s>>>(
-        a.boff, a.bidx, a.bcost, a.doff, a.didx, a.dcost, a.boff_new, a.bidx_new, a.bcost_new, a.n);
+        a.boff, a.bidx, a.bcost, a.doff, a.didx, a.dcost, a.boff_new, a.bidx_new, a.bcost_new, a.n,
+        a.own_n, a.own_r);
     return cudaGetLastError();
 }
 

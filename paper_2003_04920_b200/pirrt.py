@@ -38,6 +38,7 @@ PIRRT_F_DEVICE_PTRS = 8
 PIRRT_F_SHARDED = 16
 PIRRT_F_PARENT_FORM = 32
 PIRRT_F_NEIGHBOURS = 64
+PIRRT_F_LOCAL_GROUP = 128
 NCCL_UNIQUE_ID_BYTES = 128
 
 # every symbol include/pirrt.h declares (checked by tests/test_abi.py)
@@ -45,7 +46,7 @@ EXPORTS = (
     "pirrt_config_init", "pirrt_create", "pirrt_destroy", "pirrt_graph_append_batch",
     "pirrt_exploit", "pirrt_exploit_async", "pirrt_exploit_wait", "pirrt_get_policy",
     "pirrt_get_costs", "pirrt_get_promising", "pirrt_get_parent_costs", "pirrt_get_in_edges", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
-    "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id",
+    "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id", "pirrt_group_exploit",
     "pirrt_set_world", "pirrt_extend_batch", "pirrt_get_points",
     # include/pirrt_bench.h (measurement helpers)
     "pirrt_bench_rows", "pirrt_bench_relax", "pirrt_bench_gather",
@@ -133,6 +134,7 @@ def _load():
     lib.pirrt_kernel_launches.restype = C.c_int64
     lib.pirrt_last_error.restype = C.c_char_p
     lib.pirrt_nccl_unique_id.argtypes = [P, C.c_int64]
+    lib.pirrt_group_exploit.argtypes = [P, C.c_int32, P]
     lib.pirrt_bench_rows.argtypes = [P, P, P, P, C.c_int32, C.c_int32, P]
     lib.pirrt_bench_gather.argtypes = [P, P, C.c_int64, C.c_int32, P]
     lib.pirrt_bench_relax.argtypes = [P, P, P, P, P, C.c_int32, P, C.c_int32, P]
@@ -164,6 +166,7 @@ pirrt_num_edges = _lib.pirrt_num_edges
 pirrt_kernel_launches = _lib.pirrt_kernel_launches
 pirrt_last_error = _lib.pirrt_last_error
 pirrt_nccl_unique_id = _lib.pirrt_nccl_unique_id
+pirrt_group_exploit = _lib.pirrt_group_exploit
 
 
 def bench_rows(off, idx, cost, order, reps=5) -> float:
@@ -263,6 +266,16 @@ def _check_device_tensors(device: int, sizes: dict, **tensors):
             raise PirrtError(PIRRT_E_INVAL, f"{name}: on {t.device}, the context is on cuda:{device}")
         if name in sizes and int(t.numel()) != sizes[name]:
             raise PirrtError(PIRRT_E_INVAL, f"{name}: {t.numel()} elements, expected {sizes[name]}")
+
+
+def group_exploit(contexts) -> list:
+    """pirrt_group_exploit over an in-process group (contexts[i] = rank i,
+    created with nranks=len(contexts), rank=i, flags |= PIRRT_F_LOCAL_GROUP)."""
+    n = len(contexts)
+    hs = (C.c_void_p * n)(*[c._h for c in contexts])
+    st = (pirrt_exploit_stats * n)()
+    _check(pirrt_group_exploit(hs, n, st))
+    return [ExploitStats(*(getattr(x, f[0]) for f in pirrt_exploit_stats._fields_)) for x in st]
 
 
 class Context:
@@ -418,7 +431,8 @@ class Context:
         cost = np.empty(max(E, 1), np.float64)
         _check(pirrt_get_in_edges(self._h, off.ctypes.data, n + 1, src.ctypes.data,
                                   cost.ctypes.data, E))
-        return off, src[:E], cost[:E]
+        k = int(off[-1])                # this rank's share on a partitioned sharded store
+        return off, src[:k], cost[:k]
 
     def state(self):
         """(parent, g, pc, b) -- same order as the oracle's state()."""

@@ -84,3 +84,50 @@ def dual_replay(gpu, orc, graph, S, n_stop=None, undirected=True, check_every=1,
     opath, ocost, ogoal = orc.best_path_goal()
     assert np.array_equal(gpath, opath) and gcost == ocost and ggoal == ogoal
     return k_ex
+
+
+class RankGroup:
+    """P contexts of one in-process group (PIRRT_F_LOCAL_GROUP) driven SPMD,
+    with the Context interface dual_replay uses: every append goes to every
+    rank; exploit() runs pirrt_group_exploit and returns rank 0's stats with
+    the per-rank shares (relaxations, improve_set) summed -- after checking
+    that every rank reports the same loop counters; state() checks that every
+    rank holds the same bits and returns rank 0's."""
+
+    LOOP_KEYS = ("iterations", "evaluations", "eval_visits", "max_level", "promising", "stalled")
+
+    def __init__(self, P, nranks, stream=None, **kw):
+        self.P = P
+        flags = kw.pop("flags", 0) | P.PIRRT_F_LOCAL_GROUP
+        self.ranks = [P.Context(nranks=nranks, rank=r, flags=flags, stream=stream, **kw)
+                      for r in range(nranks)]
+
+    @property
+    def n(self):
+        return self.ranks[0].n
+
+    def append(self, *args, **kw):
+        got = [c.append(*args, **kw) for c in self.ranks]
+        assert len(set(got)) == 1, got
+        return got[0]
+
+    def exploit(self):
+        import dataclasses
+        sts = self.P.group_exploit(self.ranks)
+        for k in self.LOOP_KEYS:
+            vals = {getattr(s, k) for s in sts}
+            assert len(vals) == 1, (k, vals)
+        assert len({np.float64(s.last_delta_g).view(np.uint64) for s in sts}) == 1
+        return dataclasses.replace(sts[0], relaxations=sum(s.relaxations for s in sts),
+                                   improve_set=sum(s.improve_set for s in sts))
+
+    def state(self):
+        ref = self.ranks[0].state()
+        for c in self.ranks[1:]:
+            for name, x, y in zip(("parent", "g", "pc", "b"), c.state(), ref):
+                assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8)), \
+                    f"rank state {name} differs"
+        return ref
+
+    def best_path_goal(self):
+        return self.ranks[0].best_path_goal()

@@ -5,6 +5,7 @@ set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 export PIRRT_WATCHDOG_MS=20000
+bash tools/gpu_debug.sh
 timeout 1800 python -m pytest -m gpu -q --timeout 240 --timeout-method thread -rf --durations 20 \
     ${@:-tests} > gpurun_out/pytest_gpu.log 2>&1
 tail -45 gpurun_out/pytest_gpu.log
