@@ -173,8 +173,9 @@ struct pirrt_ctx {
     int* alist = nullptr;                                // task list
     int64_t dcap = 0;                                    // entries per dirty / g-changed buffer
     int inc_imp = 1;                                     // PIRRT_INC_IMPROVE (0 off, 1 auto, 2 always)
-    int small_grid = 0;                                  // PIRRT_SMALL_GRID: blocks for small exploits (0 off)
-    int64_t small_max = 4096;                            // PIRRT_SMALL_MAX: |B| + appended vertices bound
+    int small_grid = -1;                                 // PIRRT_SMALL_GRID: blocks for small exploits
+                                                         // (-1: one per SM; 0: off)
+    int64_t small_max = 65536;                           // PIRRT_SMALL_MAX: |B| + appended vertices bound
     int64_t n_last_exploit = 0;                          // |V| at the last exploit's launch
     int x_blocks = 0;                                    // grid of the running exploit
     int inc_max = 8192;                                  // PIRRT_INC_MAX (0: full Evaluates only)
@@ -281,7 +282,7 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
     // parity), dcap = cap + 64 entries per buffer; the incremental Improve's
     // task list: cap entries
     const int64_t dcap = cap + 64;
-    const size_t sz_ccd = al(8 * cap), sz_dirty = al(4 * 2 * dcap), sz_al = al(4 * cap);
+    const size_t sz_ccd = al(8 * cap), sz_dirty = al(4 * 2 * dcap), sz_al = al(4 * 2 * cap);
     const size_t total = sz_g + sz_pc + sz_h + sz_par + 3 * sz_st + 2 * sz_bq + sz_b + sz_ccd +
                          2 * sz_dirty + sz_al;
     char* slab = nullptr;
@@ -574,7 +575,7 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (const char* w = std::getenv("PIRRT_INC_MAX")) c->inc_max = std::max(0, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_INC_VALIDATE")) c->inc_validate = std::atoi(w) != 0;
     if (const char* w = std::getenv("PIRRT_INC_IMPROVE")) c->inc_imp = std::max(0, std::atoi(w));
-    if (const char* w = std::getenv("PIRRT_SMALL_GRID")) c->small_grid = std::max(0, std::atoi(w));
+    if (const char* w = std::getenv("PIRRT_SMALL_GRID")) c->small_grid = std::max(-1, std::atoi(w));
     if (const char* w = std::getenv("PIRRT_SMALL_MAX")) c->small_max = std::max(0, std::atoi(w));
     auto bail = [&](int rc) { free_all(c); delete c; return rc; };
     if (cfg.stream) {
@@ -600,6 +601,10 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     c->grid_blocks = cfg.grid_blocks > 0 ? std::min(cfg.grid_blocks, per_sm * c->num_sms)
                                          : per_sm * c->num_sms;
     c->grid_blocks = std::min(c->grid_blocks, kMaxGridBlocks);
+    // per-batch exploits are grid-barrier bound: one block per SM measured
+    // 10% faster than two at the bench workload and 14% at configs[1]
+    // (tools/grid_probe.py, profiles/r2/grid_probe.jsonl)
+    if (c->small_grid < 0) c->small_grid = c->num_sms;
     int rc;
     int64_t vcap0 = std::max<int64_t>(cfg.vertex_capacity, 1024);
     if ((rc = ensure_vertices(c, vcap0))) return bail(rc);
@@ -836,6 +841,7 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a, int blocks) {
     a.stamp = c->stamp;
     a.pstamp = c->pstamp; a.ccd = c->ccd; a.dirty = c->dirty;
     a.istamp = c->istamp; a.gcl = c->gcl; a.alist = c->alist; a.dcap = (int)c->dcap;
+    a.acap = (int)c->g_cap;                               // (the hot slab's vertex capacity)
     a.inc_max = (int)std::min<int64_t>(c->inc_max, c->dcap - 64);
     a.inc_imp = c->inc_imp;
     a.inc_validate = c->inc_validate;

@@ -127,6 +127,12 @@ struct DevCtl {
     int L_imp;                        // B-list length at the last Improve
     int n_imp;                        // |V| at the last Improve
     int c_buf, c_n;                   // its commits: dirty list c_buf, entries [0, c_n)
+    // task list of Improve k prebuilt by the incremental Evaluate before it
+    // (slot k & 1; alist + (k & 1) * acap): entries and the full Improve's
+    // counters over I (Sum of in-degrees, |I|)
+    alignas(128) int pre_count[2];
+    alignas(128) long long pre_relax[2];
+    alignas(128) int pre_tasks[2];
 };
 
 // Everything the persistent exploit kernel touches.
@@ -156,7 +162,8 @@ struct ExploitArgs {
     int* gcl;                     // g changed by the Evaluate after Improve k: gcl + (k & 1) * dcap
     int dcap;                     // capacity of each dirty / gcl buffer
     unsigned* istamp;             // k: the incremental Improve k has v in its task list
-    int* alist;                   // that task list
+    int* alist;                   // that task list: Improve k's at alist + (k & 1) * acap
+    int acap;
     int inc_max;                  // incremental Evaluate when its start items <= this (0: never)
     int inc_imp;                  // incremental Improve: 0 never, 1 when its sources are small
                                   // next to |I| (default), 2 whenever valid (PIRRT_INC_IMPROVE)

@@ -284,6 +284,11 @@ class Context:
     def __init__(self, h_root=0.0, h_goal=0.0, epsilon=0.0, max_iterations=0, flags=0, device=0,
                  stream=None, vertex_capacity=0, edge_capacity=0, grid_blocks=0, nranks=1,
                  rank=0, nccl_id: bytes | None = None, goals=None):
+        if (int(nranks) > 1 or int(flags) & PIRRT_F_SHARDED) and not int(flags) & PIRRT_F_LOCAL_GROUP:
+            # libpirrt dlopens libnccl.so.2: let torch load its own build of
+            # it first (same soname), so that a later `import torch` does not
+            # bind to a different NCCL
+            import torch  # noqa: F401
         cfg = pirrt_config()
         pirrt_config_init(C.byref(cfg))
         cfg.h_root, cfg.h_goal, cfg.epsilon = float(h_root), float(h_goal), float(epsilon)

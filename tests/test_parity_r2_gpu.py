@@ -236,3 +236,31 @@ def test_edges_between_old_vertices(P, monkeypatch, mode):
         orc.append(z, s[cut:], t[cut:], c[cut:], flags=U)
         assert_same_stats(gpu.exploit(), orc.exploit(), f"batch {k} (old-old edges)")
     assert_same_state(gpu, orc, "final")
+
+
+@pytest.mark.parametrize("env", [{"PIRRT_SMALL_GRID": "0"}, {"PIRRT_SMALL_GRID": "7"},
+                                 {"PIRRT_INC_VALIDATE": "1"},
+                                 {"PIRRT_SMALL_GRID": "1", "PIRRT_INC_VALIDATE": "1"}])
+@pytest.mark.parametrize("d,n,S", [(6, 12000, 500), (2, 8000, 1)])
+def test_prebuilt_task_lists_and_small_grid(P, monkeypatch, env, d, n, S):
+    """The incremental Evaluate builds the next Improve's task list (no
+    discovery phase), also through the validation fixpoint's recount
+    (PIRRT_INC_VALIDATE); small exploits run on the one-block-per-SM grid
+    (default), on 7 or 1 blocks, or on the full grid (0): identical to the
+    oracle, and the incremental Improve is used."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    gm = gen.gamma_k(d) if d > 2 else gen.gamma_star(d)
+    r = gen.rrg(d, n, gm, n_boxes=10, seed=gen.seed_of("prebuilt", d, S))
+    gpu = P.Context(h_root=r.h_root())
+    orc = Oracle(h_root=r.h_root())
+    stats = []
+    orig = gpu.exploit
+
+    def rec():
+        s = orig()
+        stats.append(s)
+        return s
+    gpu.exploit = rec
+    dual_replay(gpu, orc, r, S, n_stop=min(n, 2 + 300 * S))
+    assert sum(s.inc_improves for s in stats) > 0

@@ -34,8 +34,18 @@ MUTATIONS = [
      "std::fill(c->b.begin(), c->b.end(), 0);  // B <- {} (P:256)", ""),
     ("child test with <= (P:263)", ": (c->g[v] + c->h[v] < thr);", ": (c->g[v] + c->h[v] <= thr);"),
     ("Delta g as the last vertex's delta (R1 literal)", "if (d > dg) dg = d;", "dg = d;"),
-    ("goal not always improved (R4)", "if (!(prune_off || c->b[v] || is_goal(c, v))) continue;",
-     "if (!(prune_off || c->b[v])) continue;"),
+    ("goal not always improved (R4)",
+     "if (!(prune_off || c->b[v] || is_goal(c, v) || (!nbr.empty() && nbr[v]))) continue;",
+     "if (!(prune_off || c->b[v] || (!nbr.empty() && nbr[v]))) continue;"),
+    ("NEIGHBOURS: the root is not a source (R16)",
+     "if (uc.first == kRoot || c->b[uc.first]) { nbr[v] = 1; break; }",
+     "if (c->b[uc.first]) { nbr[v] = 1; break; }"),
+    ("NEIGHBOURS: only the root is a source (R16)",
+     "if (uc.first == kRoot || c->b[uc.first]) { nbr[v] = 1; break; }",
+     "if (uc.first == kRoot) { nbr[v] = 1; break; }"),
+    ("NEIGHBOURS: neighbours never join I (R16)",
+     "if (!(prune_off || c->b[v] || is_goal(c, v) || (!nbr.empty() && nbr[v]))) continue;",
+     "if (!(prune_off || c->b[v] || is_goal(c, v))) continue;"),
     ("local relaxation keeps the highest id on ties (R14, R6)",
      "if (cand < best || (cand == best && arg >= 0 && u < arg)) {",
      "if (cand < best || (cand == best && arg >= 0 && u > arg)) {"),
@@ -47,7 +57,7 @@ MUTATIONS = [
 ]
 
 PIN_TESTS = ["tests/test_oracle_loop_pins.py", "tests/test_oracle_pins.py",
-             "tests/test_oracle_goals_variants.py"]
+             "tests/test_oracle_goals_variants.py", "tests/test_oracle_neighbours.py"]
 
 
 def main():
