@@ -466,6 +466,19 @@ def gamma_star_record(a, peak, peak_src, K=10):
                    "mean_degree": round(ctx.n_edges / ctx.n, 2), "build_s": round(t_build, 2),
                    "roofline": roofline_of([st], peak, peak_src,
                                            "exploit_kernel + improve_wide_kernel (cold solve)")}
+    # NEXT-3 (edge-balanced Improve) evidence: the Improve phases of
+    # the cold solve (almost all in improve_wide_kernel: |I| = |V| twice) in
+    # 20 B relaxation units against the relaxation microbenchmark (rows in
+    # random order + g gathers + a min per row) on this very graph
+    mb_ms, mb_entries = pirrt.bench_relax_ctx(ctx, reps=3)
+    imp_gbps = st.relax_work * B_RELAX / (st.improve_ms * 1e-3) / 1e9
+    mb_gbps = mb_entries * B_RELAX / (mb_ms * 1e-3) / 1e9
+    rec["cold"]["improve_vs_microbench"] = {
+        "improve_GBps": round(imp_gbps, 1), "relax_microbench_GBps": round(mb_gbps, 1),
+        "ratio": round(imp_gbps / mb_gbps, 3), "microbench_entries": mb_entries,
+        "microbench_ms": round(mb_ms, 3),
+        "note": "20 B per relaxation in both; improve_ms = device time inside the Improve "
+                "phases of the cold solve"}
     del ctx, dpts
     torch.cuda.empty_cache()
     return rec

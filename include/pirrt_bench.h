@@ -22,6 +22,13 @@ int pirrt_bench_rows(const long long* off, const int* idx, const double* cost, c
 int pirrt_bench_relax(const long long* off, const int* idx, const double* cost, const double* g,
                       const int* order, int32_t nrows, double* out, int32_t reps, float* ms_out);
 
+/* The same relaxation pass over a context's own base CSR (rows in a fixed
+ * pseudo-random order, g = the context's cost-to-come): the achievable rate
+ * on exactly the graph the exploit runs on.  *entries_out = entries per pass.
+ * Runs on the context's device after completing its pending work. */
+typedef struct pirrt_ctx pirrt_ctx;
+int pirrt_bench_relax_ctx(const pirrt_ctx* ctx, int32_t reps, float* ms_out, int64_t* entries_out);
+
 /* n random 8-byte gathers src[idx[i]] (idx streamed): 4 B + one 8 B gather each. */
 int pirrt_bench_gather(const double* src, const int* idx, int64_t n, int32_t reps, float* ms_out);
 

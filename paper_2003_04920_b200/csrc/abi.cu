@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "pirrt_bench.h"
 
 using namespace pirrt;
 
@@ -1314,6 +1315,25 @@ int pirrt_get_in_edges(const pirrt_ctx* cc, int64_t* off_out, int64_t cap_v, pir
     }
     off_out[n] = k;
     if (k != Eb + Ed) return fail(PIRRT_E_CORRUPT, "get_in_edges: row offsets disagree with the edge count");
+    return PIRRT_OK;
+}
+
+int pirrt_bench_relax_ctx(const pirrt_ctx* cc, int32_t reps, float* ms_out, int64_t* entries_out) {
+    pirrt_ctx* c = const_cast<pirrt_ctx*>(cc);
+    if (!c || !ms_out || reps < 1) return fail(PIRRT_E_INVAL, "bench_relax_ctx: bad arguments");
+    int rc;
+    if ((rc = set_device(c))) return rc;
+    if ((rc = complete_pending(c))) return rc;
+    CU(cudaStreamSynchronize(c->stream));
+    double* out = nullptr;
+    if (cudaMalloc(&out, (size_t)std::max(c->n, 1) * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PIRRT_E_NOMEM, "bench_relax_ctx: scratch");
+    }
+    const int r = pirrt_bench_relax(c->boff, c->bidx, c->bcost, c->g, nullptr, c->n, out, reps, ms_out);
+    cudaFree(out);
+    if (r) return fail(PIRRT_E_CUDA, "bench_relax_ctx: kernel failed");
+    if (entries_out) *entries_out = c->base_edges;
     return PIRRT_OK;
 }
 

@@ -35,7 +35,9 @@ __global__ void k_relax(const long long* __restrict__ off, const int* __restrict
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     for (int r = w; r < nrows; r += nw) {
-        const int v = order[r];
+        // order == nullptr: a fixed pseudo-random permutation (2^31 - 1 is
+        // prime and larger than nrows)
+        const int v = order ? order[r] : (int)(((long long)r * 2147483647LL) % nrows);
         const long long k0 = __ldg(&off[v]), k1 = __ldg(&off[v + 1]);
         double best = 1e300;
         for (long long k = k0 + lane; k < k1; k += 32) {

@@ -49,7 +49,7 @@ EXPORTS = (
     "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id", "pirrt_group_exploit",
     "pirrt_set_world", "pirrt_extend_batch", "pirrt_get_points",
     # include/pirrt_bench.h (measurement helpers)
-    "pirrt_bench_rows", "pirrt_bench_relax", "pirrt_bench_gather",
+    "pirrt_bench_rows", "pirrt_bench_relax", "pirrt_bench_gather", "pirrt_bench_relax_ctx",
 )
 
 
@@ -138,6 +138,7 @@ def _load():
     lib.pirrt_bench_rows.argtypes = [P, P, P, P, C.c_int32, C.c_int32, P]
     lib.pirrt_bench_gather.argtypes = [P, P, C.c_int64, C.c_int32, P]
     lib.pirrt_bench_relax.argtypes = [P, P, P, P, P, C.c_int32, P, C.c_int32, P]
+    lib.pirrt_bench_relax_ctx.argtypes = [P, C.c_int32, P, P]
     return lib
 
 
@@ -184,6 +185,15 @@ def bench_relax(off, idx, cost, g, order, out, reps=5) -> float:
                                   order.data_ptr(), int(order.numel()), out.data_ptr(), int(reps),
                                   C.byref(ms)))
     return float(ms.value)
+
+
+def bench_relax_ctx(ctx, reps=5):
+    """(ms per pass, entries per pass) of the relaxation microbenchmark over
+    the context's own base CSR (pirrt_bench_relax_ctx)."""
+    ms = C.c_float(0)
+    ent = C.c_int64(0)
+    _check(_lib.pirrt_bench_relax_ctx(ctx._h, int(reps), C.byref(ms), C.byref(ent)))
+    return float(ms.value), int(ent.value)
 
 
 def bench_gather(src, idx, reps=5) -> float:
