@@ -666,10 +666,12 @@ def main_cuda_single(a):
 
 def main_sharded(a, rank, world):
     """configs[4]: the 10M-vertex 6-D gamma_k RRG, every rank building the
-    same graph with the device-side Extend (replicated store), exploits
-    sharded over the ranks (Improve split by vertex, NCCL all-gather of the
-    records per PI iteration, replicated Evaluate).
-    Step = one S-batch extend + exploit; the cold solve is a sub-record."""
+    same graph with the device-side Extend, exploits sharded over the ranks
+    (Improve split by vertex, one NCCL all-gather of the records per PI
+    iteration, replicated Evaluate, in-edge rows kept by their owner after a
+    fold).  Step = one S-batch extend (device points) +
+    exploit; the cold solve is a sub-record; e2e = the same steps with the
+    points copied from pinned host memory and the best path read back."""
     import torch
     import torch.distributed as dist
     import gen
@@ -685,7 +687,7 @@ def main_sharded(a, rank, world):
         kw = {}
     d, n, S, W, K = a.d, a.n, a.S, a.warmup, a.steps
     gm = gen.gamma_k(d)
-    n_all = n + (W + K) * S
+    n_all = n + (W + 2 * K) * S
     pts, bx = gen.points(d, n_all, a.boxes, seed=gen.seed_of(workload_name(a), a.seed))
     h_root = float(np.sqrt(((pts[0] - pts[1]) ** 2).sum()))
     dpts = torch.from_numpy(pts).cuda()
@@ -711,6 +713,7 @@ def main_sharded(a, rank, world):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
+            l0 = ctx.kernel_launches
         hi = lo + S
         ev[i][0].record()
         nprom, _ = ctx.extend(dpts[lo:hi])
@@ -720,26 +723,32 @@ def main_sharded(a, rank, world):
             stats.append(st)
         lo = hi
     torch.cuda.synchronize()
+    launches = ctx.kernel_launches - l0
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    # e2e: the next K batches through the same calls, points from pinned host
+    # memory (H2D inside pirrt_extend_batch), best path read back every step
+    host = torch.from_numpy(pts[lo:lo + K * S]).pin_memory().numpy()
+    h2d = d2h = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(K):
+        chunk = host[i * S:(i + 1) * S]
+        nprom, _ = ctx.extend(chunk)
+        if nprom > 0:
+            ctx.exploit()
+        path, _ = ctx.best_path()
+        h2d += chunk.nbytes
+        d2h += path.nbytes + 16
+    e1.record()
+    torch.cuda.synchronize()
     step_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(W, W + K)]
-    t = torch.tensor([sum(step_ms), cold.device_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)          # max over ranks
-    total_ms, cold_ms = float(t[0]), float(t[1])
     ex = [s for s in stats if s is not None]
-    if rank == 0:
-        peak, peak_src = peaks()
-        relax_all = sum(s.relaxations for s in ex)          # rank shares summed below
-        r = torch.tensor([float(relax_all), float(cold.relaxations)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(r, op=dist.ReduceOp.SUM)
-    else:
-        r = torch.tensor([float(sum(s.relaxations for s in ex)), float(cold.relaxations)],
-                         dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(r, op=dist.ReduceOp.SUM)
+    # the slowest rank's device times; the ranks' relaxation shares summed
+    total_ms, cold_ms, e2e_ms = pdist.max_over_ranks([sum(step_ms), cold.device_ms,
+                                                      e0.elapsed_time(e1)])
+    relax, relax_cold = pdist.sum_over_ranks([sum(s.relaxations for s in ex), cold.relaxations])
     if rank == 0:
         ms_step = total_ms / K
         line = {
@@ -752,11 +761,14 @@ def main_sharded(a, rank, world):
                        "directed_edges_stored": ctx.n_edges,
                        "step": "extend(S points, device) + exploit-to-convergence (sharded)",
                        "parallelism": f"sharded{world}" if world > 1 else "single"},
-            "gteps": round(float(r[0]) / (total_ms * 1e-3) / 1e9, 4),
+            "gteps": round(relax / (total_ms * 1e-3) / 1e9, 4),
             "cold_solve": {"exploit_ms": round(cold_ms, 4), "iterations": cold.iterations,
-                           "gteps": round(float(r[1]) / (cold_ms * 1e-3) / 1e9, 3)},
+                           "gteps": round(relax_cold / (cold_ms * 1e-3) / 1e9, 3)},
             "build_s": round(t_build, 2), "clocks": clk, "cpu_baseline": None,
-            "e2e": None, "gpu_launches": None,
+            "e2e": {"value": round(e2e_ms / K, 4), "unit": "ms", "h2d_bytes_per_step": h2d // K,
+                    "d2h_bytes_per_step": d2h // K,
+                    "mode": "extend from pinned host points + exploit + best_path, synchronous"},
+            "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -835,8 +847,8 @@ def main_reference(a, rank, world):
 def main():
     a = parse()
     spawn_if_needed(a)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+    from paper_2003_04920_b200.dist import env_rank_world
+    rank, world, _ = env_rank_world()
     if a.impl == "reference":
         return main_reference(a, rank, world)
     a = resolve(a, world)

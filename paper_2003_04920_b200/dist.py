@@ -23,29 +23,27 @@ def broadcast_unique_id(make_id, group=None) -> bytes:
     return obj[0]
 
 
-def owner(v: int, nranks: int) -> int:
-    """Rank whose Improve handles vertex v (vertex-cyclic split; stable as the graph grows)."""
-    return v % nranks
-
-
-def max_over_ranks(x: float, group=None) -> float:
-    """Max of a float over all ranks (the bench's timing rule)."""
+def _reduce(xs, op, group=None):
     import torch
     import torch.distributed as dist
+    xs = [float(x) for x in xs]
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
-        return float(x)
+        return xs
     dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-    return float(t.item())
+    t = torch.tensor(xs, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op, group=group)
+    return [float(v) for v in t.tolist()]
 
 
-def sum_over_ranks(x: float, group=None) -> float:
-    import torch
+def max_over_ranks(xs, group=None) -> list:
+    """Element-wise max over all ranks (the bench's timing rule: the slowest
+    rank's device time)."""
     import torch.distributed as dist
-    if not dist.is_initialized() or dist.get_world_size(group) == 1:
-        return float(x)
-    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return float(t.item())
+    return _reduce(xs, dist.ReduceOp.MAX, group)
+
+
+def sum_over_ranks(xs, group=None) -> list:
+    """Element-wise sum over all ranks (per-rank shares of the relaxation
+    counts -> the job's total)."""
+    import torch.distributed as dist
+    return _reduce(xs, dist.ReduceOp.SUM, group)
