@@ -638,6 +638,18 @@ def main_cuda_single(a):
         "max_level": max([s.max_level for s in ex] or [0]),
         "phase_ms": {"improve": round(imp_ms, 4), "evaluate": round(sum(s.evaluate_ms for s in ex), 4)},
         "grid_barriers_per_exploit": round(c["barriers"] / max(1, len(ex)), 1),
+        # a per-batch exploit is latency-bound (dependent
+        # phases x phase latency), so the phase breakdown goes beside the
+        # bandwidth fraction
+        "latency_breakdown": {
+            "phases_per_exploit": round(c["barriers"] / max(1, len(ex)), 2),
+            "us_per_phase": round(1e3 * ex_ms / max(1, c["barriers"]), 2),
+            "improve_us_per_iteration": round(1e3 * imp_ms / max(1, c["iterations"]), 2),
+            "evaluate_us_per_evaluation": round(1e3 * sum(s.evaluate_ms for s in ex) /
+                                                max(1, c["evaluations"]), 2),
+            "bytes_floor_us_per_exploit": round(1e6 * sum(algo_bytes(s) for s in ex) /
+                                                max(1, len(ex)) / (peak * 1e9), 2),
+        },
         "roofline": rl,
         "overhead": {"eval_scanned_entries": c["eval_scanned"],
                      "note": "out-row entries scanned to find children (8 B each), not a 8(d) unit"},

@@ -1579,6 +1579,14 @@ int pirrt_get_points(const pirrt_ctx* c, double* out, int64_t cap) {
 }  // extern "C"
 
 // ---- debug-only export (not part of include/pirrt.h): the device B list
+// diagnostics (not part of the ABI header): the last exploit's phase
+// timeline, DevCtl::phase_ns
+extern "C" int pirrt_debug_phases(const pirrt_ctx* c, unsigned long long* out, int n) {
+    if (!c || !out || n < 8) return fail(PIRRT_E_INVAL, "debug_phases: bad arguments");
+    std::memcpy(out, c->ctl_host->phase_ns, 8 * sizeof(unsigned long long));
+    return PIRRT_OK;
+}
+
 extern "C" int pirrt_debug_blist(const pirrt_ctx* c, int32_t* out, int64_t cap, int32_t* count) {
     if (!c || !out || !count) return fail(PIRRT_E_INVAL, "debug_blist: NULL");
     int rc;

@@ -94,6 +94,12 @@ struct DevCtl {
     long long relax_work, improve_work;   // relaxations / vertices actually scanned by Improve
     int full_imps, inc_imps;      // Improves run in full / incremental form
     unsigned long long t_improve, t_evaluate;
+    // phase timeline (lead thread, %globaltimer ns between grid barriers;
+    // pirrt_debug_phases): 0 Improve discovery, 1 Improve scan, 2 incremental
+    // Evaluate E2 (walk-ups + traversal), 3 its E3 (bookkeeping + next task
+    // list), 4 its validation fixpoint, 5 full Evaluates, 6 incremental
+    // Evaluates (count), 7 in-kernel Improves (count)
+    unsigned long long phase_ns[8];
     unsigned long long dbg_work_ns;   // PIRRT_DEBUG level trace
     unsigned long long dbg[8];        // PIRRT_LEVEL_TRACE work-queue counters
     unsigned long long dbg_imp[6];    // PIRRT_LEVEL_TRACE Improve timeline
