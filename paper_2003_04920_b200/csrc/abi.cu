@@ -85,6 +85,7 @@ struct NcclApi {
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char* (*errorString)(ncclResult_t) = nullptr;
     ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;   // optional
+    ncclResult_t (*commAbort)(ncclComm_t) = nullptr;                           // optional
 };
 
 NcclApi* nccl_api() {
@@ -104,6 +105,7 @@ NcclApi* nccl_api() {
             api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
             api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
             api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+            api.commAbort = (decltype(api.commAbort))dlsym(h, "ncclCommAbort");
             if (api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy &&
                 api.errorString)
                 api.h = h;
@@ -1046,6 +1048,12 @@ int exploit_launch(pirrt_ctx* c) {
         if (!c->comm) return fail(PIRRT_E_STATE, "exploit: an in-process group rank runs only through pirrt_group_exploit");
         std::vector<pirrt_ctx*> cs{c};
         c->x_rc = exploit_sharded(cs);
+        if (c->x_rc != 0 && c->x_rc != PIRRT_E_NOCONV && c->nranks > 1) {
+            // a rank that fails on its own (e.g. an allocation) must not leave
+            // its peers blocked in the next all-gather: abort the communicator
+            NcclApi* api = nccl_api();
+            if (api && api->commAbort) { api->commAbort(c->comm); c->comm = nullptr; }
+        }
         if (c->x_rc != 0 && c->x_rc != PIRRT_E_NOCONV) { c->broken = true; return c->x_rc; }
         CU(cudaEventRecord(c->ev1, s));
         return 0;

@@ -105,3 +105,27 @@ def test_so_is_sm100a():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+@pytest.mark.parametrize("case", ["nbr_sharded", "nbr_group", "nbr_nranks", "group_with_id",
+                                  "nranks_without_id"])
+def test_config_combinations_refused_without_gpu(case):
+    # configuration errors are reported before any CUDA call (runs on CPU)
+    from paper_2003_04920_b200 import pirrt
+    cfg = pirrt.pirrt_config()
+    pirrt.pirrt_config_init(C.byref(cfg))
+    uid = C.create_string_buffer(128)
+    if case == "nbr_sharded":
+        cfg.flags = pirrt.PIRRT_F_NEIGHBOURS | pirrt.PIRRT_F_SHARDED
+    elif case == "nbr_group":
+        cfg.flags = pirrt.PIRRT_F_NEIGHBOURS | pirrt.PIRRT_F_LOCAL_GROUP
+    elif case == "nbr_nranks":
+        cfg.flags = pirrt.PIRRT_F_NEIGHBOURS
+        cfg.nranks, cfg.rank, cfg.nccl_unique_id = 2, 0, C.cast(uid, C.c_void_p)
+    elif case == "group_with_id":
+        cfg.flags = pirrt.PIRRT_F_LOCAL_GROUP
+        cfg.nranks, cfg.rank, cfg.nccl_unique_id = 2, 1, C.cast(uid, C.c_void_p)
+    else:
+        cfg.nranks, cfg.rank = 2, 0
+    h = C.c_void_p()
+    assert pirrt.pirrt_create(C.byref(cfg), C.byref(h)) == pirrt.PIRRT_E_INVAL
