@@ -254,14 +254,29 @@ def counters(ex):
     return {k: int(sum(getattr(s, k) for s in ex)) for k in keys}
 
 
+def paper_bytes(st) -> float:
+    """The same units counted over the paper's full Improve / Evaluate (every
+    in-edge of every member of I in every iteration, every child of the full
+    traversal): the work the incremental forms skip is counted as if done."""
+    return st.relaxations * B_RELAX + st.improve_set * B_IVERT + st.eval_visits * B_VISIT
+
+
 def roofline_of(ex, peak, peak_src, kernel):
     ms = sum(s.device_ms for s in ex)
     byt = sum(algo_bytes(s) for s in ex)
     ach = byt / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    pb = sum(paper_bytes(s) for s in ex)
+    pach = pb / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
     return {"kernel": kernel, "bound": "hbm", "achieved": round(ach, 2), "peak": peak,
             "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 5),
             "algorithmic_bytes_per_launch": round(byt / max(1, len(ex))),
-            "formula": ALGO_FORMULA}
+            "formula": ALGO_FORMULA,
+            "paper_units": {"achieved": round(pach, 2), "frac": round(pach / peak, 5),
+                            "bytes_per_launch": round(pb / max(1, len(ex))),
+                            "formula": "20 B x relaxations + 40 B x improve_set + 37 B x "
+                                       "eval_visits (the paper's full-Improve / full-traversal "
+                                       "counts; an effective bandwidth: the incremental forms "
+                                       "skip most of these bytes)"}}
 
 
 # ------------------------------------------------------------------ N = 1: configs[2]
@@ -343,39 +358,33 @@ def run_cuda(a, dev):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = [e0.elapsed_time(e1) / max(1, n_sync - W1)] * (n_sync - W1)
-    # (b) pipelined through the asynchronous exploit:
-    # the H2D of batch k+1 and the host side of its append overlap the
-    # exploit of batch k; every step still copies its inputs from pinned host
-    # memory and reads back its result (stats + best path)
+    # (b) pipelined through the deferred step (SURVEY.md 8(f) NEXT-1,
+    # pirrt_step_async / pirrt_step_wait): each step's append + guarded
+    # exploit + best path is enqueued with no host synchronisation, two steps
+    # deep, so the H2D of batch k+1 overlaps the exploit of batch k; every
+    # step still copies its inputs from pinned host memory and reads back its
+    # result (stats + best path)
     rest = host_in[n_sync:]
     W2 = min(a.warmup, max(0, len(rest) - a.steps))
-    pipe = {"inflight": False}
-
-    def pipe_step(inputs):
-        nprom = ctx.append(*inputs, flags=EDGES_UNDIRECTED)   # H2D overlaps the running exploit
-        out = None
-        if pipe["inflight"]:
-            out = ctx.exploit_wait()                          # previous batch's Replan
-            pipe["inflight"] = False
-        path, cost = ctx.best_path()
-        if nprom > 0:                                         # Alg. 3 guard (R10)
-            ctx.exploit_async()
-            pipe["inflight"] = True
-        return out, path
-
+    depth = 2
     for i in range(W2):
-        pipe_step(rest[i])
+        ctx.step_async(*rest[i], flags=EDGES_UNDIRECTED)
+        if ctx.steps_outstanding >= depth:
+            ctx.step_wait()
+    while ctx.steps_outstanding:
+        ctx.step_wait()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(W2, W2 + a.steps):
-        st, path = pipe_step(rest[i])
+        ctx.step_async(*rest[i], flags=EDGES_UNDIRECTED)
         h2d += sum(x.nbytes for x in rest[i])
-        d2h += 4 + path.nbytes + 16 + (st_bytes if st else 0)
-    if pipe["inflight"]:
-        ctx.exploit_wait()
-    path, _ = ctx.best_path()
-    d2h += 4 + path.nbytes + 16 + st_bytes
+        if ctx.steps_outstanding >= depth:
+            r = ctx.step_wait()
+            d2h += 4 + r.path.nbytes + 16 + st_bytes
+    while ctx.steps_outstanding:
+        r = ctx.step_wait()
+        d2h += 4 + r.path.nbytes + 16 + st_bytes
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_pipe_ms = e0.elapsed_time(e1)
@@ -655,9 +664,11 @@ def main_cuda_single(a):
                      "note": "out-row entries scanned to find children (8 B each), not a 8(d) unit"},
         "e2e": {"value": round(res["e2e_ms"] / a.steps, 4), "unit": "ms",
                 "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"]),
-                "mode": "pipelined: append of batch k+1 (H2D from pinned host) overlaps the "
-                        "asynchronous exploit of batch k (pirrt_exploit_async); per step one "
-                        "best_path + stats read-back",
+                "mode": "pipelined: pirrt_step_async / pirrt_step_wait two steps deep (append "
+                        "+ guarded exploit + best_path enqueued with no host synchronisation; the "
+                        "H2D of batch k+1 from pinned host memory overlaps the exploit of batch "
+                        "k); per step one best path + stats read-back",
+                "sync_mode": "one synchronous call after another (append, exploit, best_path)",
                 "sync_value": round(res["e2e_sync_ms"] / max(1, res["e2e_sync_steps"]), 4)},
         "gpu_launches": int(res["launches"]),
         "clocks": res["clocks"],
@@ -865,10 +876,18 @@ def main():
         return main_reference(a, rank, world)
     a = resolve(a, world)
     if a.workload == "cfg5":
-        return main_sharded(a, rank, world)
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        with torch.cuda.stream(torch.cuda.Stream()):
+            return main_sharded(a, rank, world)
     if world > 1:
         raise SystemExit("cfg3 runs on one GPU; N > 1 runs configs[4] (--workload cfg5)")
-    return main_cuda_single(a)
+    import torch
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    # one dedicated stream for everything timed: the library's kernels, the
+    # L2 flush and the CUDA events are then ordered on the same stream
+    with torch.cuda.stream(torch.cuda.Stream()):
+        return main_cuda_single(a)
 
 
 if __name__ == "__main__":

@@ -20,8 +20,9 @@
  *     copies inputs before returning and owns all device memory.  Unless the
  *     call's flags contain PIRRT_F_DEVICE_PTRS, pointers are host pointers
  *     (pinned host memory makes the H2D copies asynchronous DMA).  Every call
- *     is synchronous with respect to the context's stream: when it returns,
- *     results are visible to the caller.
+ *     except pirrt_exploit_async and pirrt_step_async is synchronous with
+ *     respect to the context's stream: when it returns, results are visible
+ *     to the caller.
  *   - Errors: every call returns PIRRT_OK (0) or a negative PIRRT_E_* code and
  *     sets a thread-local message readable with pirrt_last_error().  On error
  *     the context state (graph, policy, costs, promising set) is unchanged,
@@ -87,7 +88,10 @@ typedef struct {
     int32_t max_iterations;   /* Improve cap per exploit; 0 -> 10 |V| (R11)                  */
     uint32_t flags;           /* PIRRT_F_PRUNE_OFF | PIRRT_F_VALIDATE | PIRRT_F_PARENT_FORM  */
     int32_t device;           /* CUDA device ordinal                                        */
-    void* stream;             /* cudaStream_t to run on (e.g. a torch stream); NULL: own one */
+    void* stream;             /* cudaStream_t to run on (e.g. a torch stream; the legacy
+                                 default stream is cudaStreamLegacy, (void*)1); NULL: the
+                                 context creates its own non-blocking stream, which does
+                                 not synchronise with the caller's default stream          */
     int32_t grid_blocks;      /* persistent-kernel grid; 0 = auto (SMs x occupancy)          */
     int32_t nranks;           /* multi-GPU SPMD: ranks (1 = single GPU), one process per GPU */
     int32_t rank;             /* this process's rank                                        */
@@ -206,6 +210,47 @@ int pirrt_exploit(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
  * pirrt_exploit_async.  E_STATE: wait without a started exploit. */
 int pirrt_exploit_async(pirrt_ctx* ctx);
 int pirrt_exploit_wait(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
+
+/* Deferred BE-RRT# step (PAPER.md:565-574,
+ * "asynchronous policy iteration exploitation concurrent with exploration").
+ * pirrt_step_async enqueues one whole iteration of Alg. 3
+ * and returns without waiting for the device:
+ *   append the batch (as pirrt_graph_append_batch with parent_new = g_new =
+ *   NULL: Extend's local relaxation, R14; flags may hold
+ *   PIRRT_F_EDGES_UNDIRECTED and PIRRT_F_DEVICE_PTRS), then Replan
+ *   (pirrt_exploit) iff the batch brought a new promising vertex (Alg. 3
+ *   line 9, R10 -- decided on the device), then the best-path
+ *   read-out (pirrt_best_path).
+ * Up to two steps may be outstanding: the H2D of step k+1's inputs overlaps
+ * step k's exploit, and the host never sits between the kernels of a step.
+ * Host inputs are read asynchronously: they must stay valid and unchanged
+ * until this step's pirrt_step_wait returns (pinned memory makes the copy a
+ * DMA).  pirrt_step_wait completes the oldest outstanding step and returns
+ * its result in *out (nullable) and its best path root..goal in
+ * path_out[0..out->path_len) (nullable; E_RANGE if cap is smaller, the rest
+ * of *out is still filled).  Results are identical to the synchronous calls.
+ * While a step is outstanding every other call returns E_STATE.
+ * Errors of step_async: E_INVAL as the append's argument checks, and
+ * PIRRT_F_VALIDATE (use the synchronous append); E_STATE two steps already
+ * outstanding, a sharded context, or a context with a world.  A batch the
+ * device rejects (an id out of range, a bad cost or h: the append's E_RANGE /
+ * E_INVAL) is reported by its pirrt_step_wait and leaves the context
+ * unusable; E_NOCONV as pirrt_exploit. */
+typedef struct {
+    int32_t n_new_promising;   /* as pirrt_graph_append_batch                          */
+    int32_t replanned;         /* 1: the exploit ran (n_new_promising > 0)              */
+    int64_t path_len;          /* best path (0: no goal reached)                        */
+    double path_cost;          /* its g (+inf: none)                                    */
+    pirrt_vid goal;            /* its goal (-1: none)                                   */
+    int32_t pad_;
+    pirrt_exploit_stats stats; /* the exploit's (zero if !replanned, except promising) */
+} pirrt_step_result;
+
+int pirrt_step_async(pirrt_ctx* ctx, int32_t n_new, const double* h_new, int64_t n_edges,
+                     const pirrt_vid* src, const pirrt_vid* dst, const double* cost,
+                     uint32_t flags);
+int pirrt_step_wait(pirrt_ctx* ctx, pirrt_step_result* out, pirrt_vid* path_out, int64_t cap);
+int pirrt_steps_outstanding(const pirrt_ctx* ctx);
 
 /* Read-out of the vertex state the paper's GPU version keeps per vertex
  * (the cost-to-come g, the parent pointer of the policy

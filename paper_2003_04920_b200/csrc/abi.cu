@@ -187,7 +187,9 @@ struct pirrt_ctx {
     // work-queue Evaluate items (slot 0 = root, the rest -1 between Evaluates)
     int* qv = nullptr; double* qg = nullptr; int* qdepth = nullptr; int64_t q_cap = 0;
     char* slab = nullptr; size_t slab_bytes = 0;          // hot per-vertex arrays (one allocation)
-    bool l2_persist = true;                              // PIRRT_L2_PERSIST=0 disables
+    bool l2_persist = false;                             // PIRRT_L2_PERSIST=1 enables (measured: no
+                                                         // exploit gain, and the carve-out halves the
+                                                         // append's streaming bandwidth)
     int64_t persist_max = 0, window_max = 0;
     L2Window l2win;
     int Bsel = 0;
@@ -228,6 +230,7 @@ struct pirrt_ctx {
     int kids_min = -1;                                       // PIRRT_KIDS_MIN: |B| for the children index
                                                              // (-1: 4 n / mean degree; 0: never)
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
+    int* app_chunk = nullptr; int64_t app_chunk_cap = 0;   // append P4 chunk rows (both deltas)
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
     // goal set G (R4): sorted unique ids incl. x_goal (device copy + host copy)
     int* goals = nullptr; int64_t goals_cap = 0;
@@ -260,13 +263,31 @@ struct pirrt_ctx {
     int* x_dst = nullptr; int64_t x_dst_cap = 0;
     double* x_cost = nullptr; int64_t x_cost_cap = 0;
     bool in_extend = false;       // the append is pirrt_extend_batch's own
+    // deferred BE-RRT# steps (pirrt_step_async / pirrt_step_wait): a ring of
+    // kStepDepth slots, each the step's read-back (control block tail, best
+    // path head) in pinned memory, its own device best-path buffer and events
+    struct StepSlot {
+        DevCtl* ctl = nullptr;            // pinned; the tail from `status` on
+        int* head = nullptr;              // pinned; best_path header + kStepHead entries
+        int* dpath = nullptr; int64_t dpath_cap = 0;
+        cudaEvent_t e0 = nullptr, e1 = nullptr, done = nullptr;
+        int blocks = 0;
+    } slot[2];
+    int steps_out = 0;            // steps enqueued and not yet waited
+    int step_head = 0;            // slot of the oldest of them
+    cudaEvent_t app_done = nullptr;   // after the last step's append (staging free again)
 };
+
+constexpr int kStepDepth = 2;
+constexpr int kStepHead = 1020;
 
 namespace {
 
-int set_device(const pirrt_ctx* c) {
+int set_device(const pirrt_ctx* c, bool steps_ok = false) {
     CU(cudaSetDevice(c->cfg.device));
     if (c->broken) return fail(PIRRT_E_STATE, "context unusable after an earlier CUDA error");
+    if (c->steps_out > 0 && !steps_ok)
+        return fail(PIRRT_E_STATE, "a deferred step is outstanding (pirrt_step_wait first)");
     return 0;
 }
 
@@ -407,6 +428,15 @@ void free_all(pirrt_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
+    if (c->app_chunk) cudaFree(c->app_chunk);
+    for (auto& sl : c->slot) {
+        if (sl.ctl) cudaFreeHost(sl.ctl);
+        if (sl.head) cudaFreeHost(sl.head);
+        if (sl.dpath) cudaFree(sl.dpath);
+        for (cudaEvent_t e : {sl.e0, sl.e1, sl.done})
+            if (e) cudaEventDestroy(e);
+    }
+    if (c->app_done) cudaEventDestroy(c->app_done);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->copy_done) cudaEventDestroy(c->copy_done);
@@ -466,7 +496,7 @@ int fold(pirrt_ctx* c, long long*& boff, int64_t& boff_cap, int*& bidx, int64_t&
     return 0;
 }
 
-int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
+int compact_if_needed(pirrt_ctx* c, int64_t m_dir, bool sync = true) {
     // fold the deltas into the bases when they outgrow sqrt(2 m |base|) (and
     // 32k edges): minimises (mean delta copied per append) + (|E| fold cost
     // amortised over the appends between folds)
@@ -498,8 +528,41 @@ int compact_if_needed(pirrt_ctx* c, int64_t m_dir) {
     c->delta_edges = 0;
     // the fold belongs to this append: finish it before returning, so that
     // it is neither hidden in nor charged to the next call on the stream
-    CU(cudaStreamSynchronize(c->stream));
+    // (a deferred step leaves it in the stream order)
+    if (sync) CU(cudaStreamSynchronize(c->stream));
     return 0;
+}
+
+// the fused append kernel's arguments (pirrt_graph_append_batch, pirrt_step_async)
+void fill_append_args(pirrt_ctx* c, AppendArgs& a, int nb, int n_old, int n_new, const double* d_h,
+                      const int* d_parent, const double* d_g, const int* d_src, const int* d_dst,
+                      const double* d_cost, int64_t n_edges, bool undirected, bool validate) {
+    std::memset(&a, 0, sizeof(a));
+    a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
+    a.doff_old = c->doff[c->cur]; a.didx_old = c->didx[c->cur]; a.dcost_old = c->dcost[c->cur];
+    a.doff_new = c->doff[nb]; a.didx_new = c->didx[nb]; a.dcost_new = c->dcost[nb];
+    a.boff_w = c->boff;
+    a.oboff = c->oboff; a.obidx = c->obidx;
+    a.odoff_old = c->odoff[c->cur]; a.odidx_old = c->odidx[c->cur];
+    a.odoff_new = c->odoff[nb]; a.odidx_new = c->odidx[nb];
+    a.oboff_w = c->oboff;
+    a.obase_edges = c->obase_edges;
+    a.Blist = c->Bq[c->Bsel]; a.Bcount = c->Bcount;
+    a.Bq0 = c->Bq[0]; a.Bq1 = c->Bq[1];
+    const int64_t nch = c->delta_edges / kAppendCopyChunk + 2;
+    a.chunk_in = c->app_chunk; a.chunk_out = c->app_chunk + nch;
+    a.cnt = c->cnt; a.scan_tmp = c->scan_tmp;
+    a.h_in = d_h; a.parent_in = d_parent; a.g_in = d_g;
+    a.src = d_src; a.dst = d_dst; a.cost = d_cost; a.m = n_edges;
+    a.undirected = undirected ? 1 : 0;
+    a.validate = validate ? 1 : 0;
+    a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
+    a.ccd = c->ccd;
+    a.n_old = n_old; a.n_new = n_new; a.base_edges = c->base_edges;
+    a.ctl = c->ctl;
+    a.grid_blocks = c->num_sms;
+    a.per_sm = c->append_per_sm;
+    a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
 }
 
 int complete_pending(pirrt_ctx* c);   // below, with the exploit
@@ -765,29 +828,12 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     CU(cudaMemsetAsync(&c->ctl->err, 0, 2 * sizeof(int), s));   // err, sweeps
     CU(cudaMemsetAsync(&c->ctl->nprom, 0, sizeof(int), s));
     CU(cudaMemsetAsync(&c->ctl->sweep_changed[0], 0, 2 * sizeof(int), s));
+    if ((rc = grow(c->app_chunk, c->app_chunk_cap, 2 * (c->delta_edges / kAppendCopyChunk + 2), 0, s)))
+        return rc;
     AppendArgs a;
-    a.boff = c->boff; a.bidx = c->bidx; a.bcost = c->bcost;
-    a.doff_old = c->doff[c->cur]; a.didx_old = c->didx[c->cur]; a.dcost_old = c->dcost[c->cur];
-    a.doff_new = c->doff[nb]; a.didx_new = c->didx[nb]; a.dcost_new = c->dcost[nb];
-    a.boff_w = c->boff;
-    a.oboff = c->oboff; a.obidx = c->obidx;
-    a.odoff_old = c->odoff[c->cur]; a.odidx_old = c->odidx[c->cur];
-    a.odoff_new = c->odoff[nb]; a.odidx_new = c->odidx[nb];
-    a.oboff_w = c->oboff;
-    a.obase_edges = c->obase_edges;
-    a.Blist = c->Bq[c->Bsel]; a.Bcount = c->Bcount;
-    a.cnt = c->cnt; a.scan_tmp = c->scan_tmp;
-    a.h_in = d_h; a.parent_in = parent_new ? d_parent : nullptr; a.g_in = g_new ? d_g : nullptr;
-    a.src = d_src; a.dst = d_dst; a.cost = d_cost; a.m = n_edges;
-    a.undirected = undirected ? 1 : 0;
-    a.validate = ((flags | c->cfg.flags) & PIRRT_F_VALIDATE) ? 1 : 0;
-    a.g = c->g; a.h = c->h; a.parent = c->parent; a.pc = c->pc; a.b = c->b;
-    a.ccd = c->ccd;
-    a.n_old = n_old; a.n_new = n_new; a.base_edges = c->base_edges;
-    a.ctl = c->ctl;
-    a.grid_blocks = c->num_sms;
-    a.per_sm = c->append_per_sm;
-    a.goals = c->goals; a.n_goals = (int)c->goals_host.size();
+    fill_append_args(c, a, nb, n_old, n_new, d_h, parent_new ? d_parent : nullptr, g_new ? d_g : nullptr,
+                     d_src, d_dst, d_cost, n_edges, undirected,
+                     ((flags | c->cfg.flags) & PIRRT_F_VALIDATE) != 0);
     const long long l0 = g_kernel_launches;
     cudaError_t e = launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks,
                                         c->l2win, s);
@@ -1076,6 +1122,32 @@ int exploit_launch(pirrt_ctx* c) {
     return 0;
 }
 
+// the exploit counters of a control-block read-back (pirrt_exploit_stats)
+void stats_from(const DevCtl& h, pirrt_exploit_stats* st, int blocks, float device_ms) {
+    std::memset(st, 0, sizeof(*st));
+    st->iterations = h.iterations;
+    st->evaluations = h.evaluations;
+    st->last_delta_g = h.last_dg;
+    st->relaxations = h.relaxations;
+    st->eval_visits = h.eval_visits;
+    st->max_level = h.max_level;
+    st->promising = h.promising;
+    st->stalled = h.stalled;
+    st->grid_blocks = blocks;
+    st->device_ms = device_ms;
+    st->improve_ms = (float)(h.t_improve * 1e-6);
+    st->evaluate_ms = (float)(h.t_evaluate * 1e-6);
+    st->improve_set = h.improve_set;
+    st->eval_scanned = h.eval_scanned;
+    st->barriers = h.barriers;
+    st->eval_work = h.work_visits;
+    st->full_evaluations = h.full_evals;
+    st->inc_evaluations = h.inc_evals;
+    st->relax_work = h.relax_work;
+    st->improve_work = h.improve_work;
+    st->inc_improves = h.inc_imps;
+}
+
 int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
     cudaStream_t s = c->stream;
     int rc;
@@ -1124,30 +1196,9 @@ int exploit_finish(pirrt_ctx* c, pirrt_exploit_stats* st) {
     }
     const DevCtl& h = *c->ctl_host;
     if (st) {
-        std::memset(st, 0, sizeof(*st));
-        st->iterations = h.iterations;
-        st->evaluations = h.evaluations;
-        st->last_delta_g = h.last_dg;
-        st->relaxations = h.relaxations;
-        st->eval_visits = h.eval_visits;
-        st->max_level = h.max_level;
-        st->promising = h.promising;
-        st->stalled = h.stalled;
-        st->grid_blocks = c->sharded ? c->shard_blocks : c->x_blocks;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
-        st->device_ms = ms;
-        st->improve_ms = (float)(h.t_improve * 1e-6);
-        st->evaluate_ms = (float)(h.t_evaluate * 1e-6);
-        st->improve_set = h.improve_set;
-        st->eval_scanned = h.eval_scanned;
-        st->barriers = h.barriers;
-        st->eval_work = h.work_visits;
-        st->full_evaluations = h.full_evals;
-        st->inc_evaluations = h.inc_evals;
-        st->relax_work = h.relax_work;
-        st->improve_work = h.improve_work;
-        st->inc_improves = h.inc_imps;
+        stats_from(h, st, c->sharded ? c->shard_blocks : c->x_blocks, ms);
     }
     if (h.abort_at) {
         c->broken = true;
@@ -1172,6 +1223,32 @@ int complete_pending(pirrt_ctx* c) {
 // A new exploit discards an unwaited kept result -- unless that result was a
 // failure (e.g. E_NOCONV of an asynchronous exploit another call completed):
 // then the new exploit is not started and the failure is reported now.
+int step_slot_init(pirrt_ctx* c, pirrt_ctx::StepSlot& sl) {
+    if (!sl.ctl) {
+        if (cudaMallocHost(&sl.ctl, sizeof(DevCtl)) != cudaSuccess ||
+            cudaMallocHost(&sl.head, sizeof(int) * (4 + kStepHead)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(PIRRT_E_NOMEM, "step_async: pinned slot");
+        }
+        CU(cudaEventCreate(&sl.e0));
+        CU(cudaEventCreate(&sl.e1));
+        CU(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
+    return grow(sl.dpath, sl.dpath_cap, c->vcap + 8, 0, c->stream);
+}
+
+// every outstanding step's kernels done; the host mirror of the B-list state
+// refreshed from the device (before a capacity growth, which copies the list)
+int drain_steps(pirrt_ctx* c) {
+    CU(cudaStreamSynchronize(c->stream));
+    int v[3];
+    CU(cudaMemcpy(v, &c->ctl->dev_Bsel, sizeof v, cudaMemcpyDeviceToHost));
+    c->Bsel = v[0];
+    c->Bcount = v[1];
+    c->ev_next = (unsigned)v[2];
+    return 0;
+}
+
 int take_kept_failure(pirrt_ctx* c) {
     if (!c->kept) return 0;
     c->kept = false;
@@ -1254,6 +1331,184 @@ int pirrt_exploit_wait(pirrt_ctx* c, pirrt_exploit_stats* st) {
     if (st) *st = c->kept_stats;
     return c->kept_rc == PIRRT_OK ? PIRRT_OK : fail(c->kept_rc, "exploit: failed (reported late)");
 }
+
+// ---- deferred BE-RRT# steps
+//
+// One call enqueues a whole step of Alg. 3 -- Extend's append,
+// the guarded Replan (R10) and the path read-out -- with
+// no host synchronisation: the inputs' H2D runs on the copy stream behind the
+// previous step's append (so it overlaps that step's exploit), the kernels
+// take the B-list state the previous step left on the device (DevCtl dev_*)
+// and the Alg. 3 guard is decided by the exploit kernel itself (nprom == 0:
+// it returns at once).  The results land in the slot's pinned buffers.
+int pirrt_step_async(pirrt_ctx* c, int32_t n_new, const double* h_new, int64_t n_edges,
+                     const pirrt_vid* src, const pirrt_vid* dst, const double* cost, uint32_t flags) {
+    if (!c) return fail(PIRRT_E_INVAL, "step_async: NULL context");
+    int rc;
+    if ((rc = set_device(c, true))) return rc;
+    if (c->steps_out >= kStepDepth) return fail(PIRRT_E_STATE, "step_async: two steps outstanding (pirrt_step_wait first)");
+    if (c->sharded) return fail(PIRRT_E_STATE, "step_async: single-GPU contexts only");
+    if (c->w_d != 0) return fail(PIRRT_E_STATE, "step_async: a context with a world grows through pirrt_extend_batch");
+    if ((flags | c->cfg.flags) & PIRRT_F_VALIDATE)
+        return fail(PIRRT_E_INVAL, "step_async: PIRRT_F_VALIDATE needs the synchronous append");
+    if (n_new < 0 || n_edges < 0) return fail(PIRRT_E_INVAL, "step_async: negative size");
+    if (n_new > 0 && !h_new) return fail(PIRRT_E_INVAL, "step_async: h_new is NULL");
+    if (n_edges > 0 && (!src || !dst || !cost)) return fail(PIRRT_E_INVAL, "step_async: NULL edge array");
+    if ((int64_t)c->n + n_new > INT32_MAX - 1) return fail(PIRRT_E_RANGE, "step_async: too many vertices");
+    if ((rc = complete_pending(c))) return rc;            // an exploit_async still running
+    if ((rc = take_kept_failure(c))) return rc;
+    const bool dev = (flags & PIRRT_F_DEVICE_PTRS) != 0;
+    const bool undirected = (flags & PIRRT_F_EDGES_UNDIRECTED) != 0;
+    const int64_t m_dir = undirected ? 2 * n_edges : n_edges;
+    cudaStream_t s = c->stream;
+    const int n_old = c->n, n_all = c->n + n_new;
+    const int nb = 1 - c->cur;
+    const int64_t dneed = c->delta_edges + m_dir;
+    // a capacity growth copies the B list by the host's count: bring the
+    // host mirror up to date first (rare: capacities grow geometrically)
+    const bool growth = n_all > c->vcap || dneed > c->didx_cap[nb] || dneed > c->dcost_cap[nb] ||
+                        dneed > c->odidx_cap[nb] ||
+                        (!dev && (n_new > c->s_h_cap || n_edges > c->s_src_cap ||
+                                  n_edges > c->s_dst_cap || n_edges > c->s_cost_cap));
+    if (growth && c->steps_out > 0 && (rc = drain_steps(c))) { c->broken = true; return rc; }
+    if ((rc = ensure_vertices(c, n_all))) return rc;
+    if ((rc = grow(c->didx[nb], c->didx_cap[nb], dneed, 0, s))) return rc;
+    if ((rc = grow(c->dcost[nb], c->dcost_cap[nb], dneed, 0, s))) return rc;
+    if ((rc = grow(c->odidx[nb], c->odidx_cap[nb], dneed, 0, s))) return rc;
+    pirrt_ctx::StepSlot& sl = c->slot[(c->step_head + c->steps_out) % kStepDepth];
+    if ((rc = step_slot_init(c, sl))) return rc;
+    if (!c->app_done) CU(cudaEventCreateWithFlags(&c->app_done, cudaEventDisableTiming));
+    // inputs: H2D on the copy stream once the previous step's append has
+    // consumed the staging buffers -- it overlaps that step's exploit
+    const double* d_h = h_new;
+    const int *d_src = src, *d_dst = dst;
+    const double* d_cost = cost;
+    if (!dev) {
+        CU(cudaStreamWaitEvent(c->copy_stream, c->app_done, 0));
+        if ((rc = stage(c, h_new, n_new, false, c->s_h, c->s_h_cap, &d_h, c->copy_stream))) return rc;
+        if ((rc = stage(c, src, n_edges, false, c->s_src, c->s_src_cap, &d_src, c->copy_stream))) return rc;
+        if ((rc = stage(c, dst, n_edges, false, c->s_dst, c->s_dst_cap, &d_dst, c->copy_stream))) return rc;
+        if ((rc = stage(c, cost, n_edges, false, c->s_cost, c->s_cost_cap, &d_cost, c->copy_stream))) return rc;
+        CU(cudaEventRecord(c->copy_done, c->copy_stream));
+        CU(cudaStreamWaitEvent(s, c->copy_done, 0));
+    }
+    // append (Extend's local relaxation and promising test, R14 / P:184-188)
+    CU(cudaMemsetAsync(&c->ctl->err, 0, 2 * sizeof(int), s));   // err, sweeps
+    CU(cudaMemsetAsync(&c->ctl->nprom, 0, sizeof(int), s));
+    CU(cudaMemsetAsync(&c->ctl->sweep_changed[0], 0, 2 * sizeof(int), s));
+    if ((rc = grow(c->app_chunk, c->app_chunk_cap, 2 * (c->delta_edges / kAppendCopyChunk + 2), 0, s)))
+        return rc;
+    AppendArgs a;
+    fill_append_args(c, a, nb, n_old, n_new, d_h, nullptr, nullptr, d_src, d_dst, d_cost, n_edges,
+                     undirected, false);
+    a.dev_list = c->steps_out > 0 ? 1 : 0;                // the list as the previous step left it
+    const long long l0 = g_kernel_launches;
+    cudaError_t e = launch_append_fused(a, c->cnt + (c->cnt_cap / 2), c->app_bsum, kAppendMaxBlocks,
+                                        c->l2win, s);
+    if (e != cudaSuccess) { c->broken = true; return fail(PIRRT_E_CUDA, std::string("step_async: append: ") + cudaGetErrorString(e)); }
+    CU(cudaEventRecord(c->app_done, s));
+    // commit the host side (a rejected batch is reported by pirrt_step_wait
+    // and leaves the context unusable)
+    c->cur = nb;
+    c->n = n_all;
+    c->delta_edges += m_dir;
+    c->edges_total += m_dir;
+    if ((rc = compact_if_needed(c, m_dir, false))) { c->broken = true; return rc; }
+    // Replan, guarded on the device (R10).  Grid size and the instantiation
+    // are chosen from the host's last known |B| plus this batch (an upper
+    // bound of its new members); neither changes the result
+    const int64_t bc_est = (int64_t)c->Bcount + n_new;
+    int blocks = c->grid_blocks;
+    if (c->small_grid > 0 && bc_est + (c->n - c->n_last_exploit) <= c->small_max)
+        blocks = std::min(c->small_grid, c->grid_blocks);
+    c->n_last_exploit = c->n;
+    ExploitArgs x;
+    fill_exploit_args(c, x, blocks);
+    x.kids_variant = kids_variant(x, (int)std::min<int64_t>(bc_est, INT32_MAX));
+    x.wide_tasks = 0;                                     // no host hand-off inside a step
+    x.it_base = 1;
+    x.step_mode = c->steps_out > 0 ? 2 : 1;
+    CU(cudaMemsetAsync(c->ctl, 0, offsetof(DevCtl, err), s));
+    CU(cudaEventRecord(sl.e0, s));
+    if ((e = launch_exploit(x, blocks, c->l2win, s)) != cudaSuccess) {
+        c->broken = true;
+        return fail(PIRRT_E_CUDA, std::string("step_async: exploit: ") + cudaGetErrorString(e));
+    }
+    CU(cudaEventRecord(sl.e1, s));
+    sl.blocks = blocks;
+    // path read-out (Alg. 1 lines 8-12) into the slot
+    CU(launch_best_path(c->parent, c->g, c->n, c->goals, (int)c->goals_host.size(), sl.dpath, s));
+    c->launches += g_kernel_launches - l0;
+    CU(cudaMemcpyAsync(sl.head, sl.dpath, sizeof(int) * (4 + kStepHead), cudaMemcpyDeviceToHost, s));
+    const size_t o = offsetof(DevCtl, status);
+    CU(cudaMemcpyAsync((char*)sl.ctl + o, (const char*)c->ctl + o, sizeof(DevCtl) - o,
+                       cudaMemcpyDeviceToHost, s));
+    CU(cudaEventRecord(sl.done, s));
+    ++c->steps_out;
+    return PIRRT_OK;
+}
+
+int pirrt_step_wait(pirrt_ctx* c, pirrt_step_result* out, pirrt_vid* path_out, int64_t cap) {
+    if (!c) return fail(PIRRT_E_INVAL, "step_wait: NULL context");
+    int rc;
+    if ((rc = set_device(c, true))) return rc;
+    if (c->steps_out == 0) return fail(PIRRT_E_STATE, "step_wait: no step outstanding");
+    pirrt_ctx::StepSlot& sl = c->slot[c->step_head];
+    CU(cudaEventSynchronize(sl.done));
+    c->step_head = (c->step_head + 1) % kStepDepth;
+    --c->steps_out;
+    const DevCtl& h = *sl.ctl;
+    if (h.err) {
+        c->broken = true;
+        return fail((h.err & kErrRange) ? PIRRT_E_RANGE : PIRRT_E_INVAL,
+                    "step: append rejected (context unusable):" + err_bits(h.err));
+    }
+    if (h.abort_at) {
+        c->broken = true;
+        return fail(PIRRT_E_STATE, "step: watchdog fired (PIRRT_WATCHDOG_MS); context unusable");
+    }
+    // the host mirror of the B-list state (exact once no step is outstanding)
+    c->Bsel = h.dev_Bsel;
+    c->Bcount = h.dev_Bcount;
+    c->ev_next = h.dev_ev;
+    pirrt_step_result r;
+    std::memset(&r, 0, sizeof r);
+    r.n_new_promising = h.nprom;
+    r.replanned = h.nprom > 0 ? 1 : 0;
+    if (r.replanned) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, sl.e0, sl.e1);
+        stats_from(h, &r.stats, sl.blocks, ms);
+    } else {
+        r.stats.promising = h.promising;
+    }
+    const int len = sl.head[0];
+    double gg;
+    std::memcpy(&gg, &sl.head[2], sizeof(double));
+    r.goal = -1;
+    r.path_cost = INFINITY;
+    if (!std::isinf(gg)) {
+        if (len <= 0) return fail(PIRRT_E_CORRUPT, "step: best path: parent cycle");
+        r.path_len = len;
+        r.path_cost = gg;
+        r.goal = sl.head[1];
+    }
+    if (out) *out = r;
+    if (r.path_len > 0 && path_out) {
+        if (cap < r.path_len) return fail(PIRRT_E_RANGE, "step_wait: path capacity too small");
+        std::vector<int> rev(len);
+        std::copy(sl.head + 4, sl.head + 4 + std::min(len, kStepHead), rev.begin());
+        if (len > kStepHead)                              // the slot's buffer stays until its reuse
+            CU(cudaMemcpy(rev.data() + kStepHead, sl.dpath + 4 + kStepHead,
+                          (size_t)(len - kStepHead) * sizeof(int), cudaMemcpyDeviceToHost));
+        if (rev.back() != kRoot) return fail(PIRRT_E_CORRUPT, "step: best path does not reach the root");
+        for (int i = 0; i < len; ++i) path_out[i] = rev[len - 1 - i];
+    }
+    if (h.status == PIRRT_E_NOCONV) return fail(PIRRT_E_NOCONV, "step: exploit iteration cap exceeded");
+    return PIRRT_OK;
+}
+
+int pirrt_steps_outstanding(const pirrt_ctx* c) { return c ? c->steps_out : 0; }
 
 int pirrt_nccl_unique_id(void* out, int64_t cap) {
     if (!out || cap < (int64_t)sizeof(ncclUniqueId)) return fail(PIRRT_E_RANGE, "nccl_unique_id: need 128 bytes");
@@ -1592,6 +1847,14 @@ int pirrt_get_points(const pirrt_ctx* c, double* out, int64_t cap) {
 extern "C" int pirrt_debug_phases(const pirrt_ctx* c, unsigned long long* out, int n) {
     if (!c || !out || n < 8) return fail(PIRRT_E_INVAL, "debug_phases: bad arguments");
     std::memcpy(out, c->ctl_host->phase_ns, 8 * sizeof(unsigned long long));
+    return PIRRT_OK;
+}
+
+// append phase timeline (DevCtl::app_ns, accumulated since create; valid
+// after a synchronous append): 12 entries
+extern "C" int pirrt_debug_append_phases(const pirrt_ctx* c, unsigned long long* out, int n) {
+    if (!c || !out || n < 12) return fail(PIRRT_E_INVAL, "debug_append_phases: bad arguments");
+    std::memcpy(out, c->ctl_host->app_ns, 12 * sizeof(unsigned long long));
     return PIRRT_OK;
 }
 

@@ -113,6 +113,12 @@ struct DevCtl {
     // append / set_policy (the words every block may update on their own lines)
     alignas(128) int err;         // bitmask of kErr*
     int sweeps;                   // local-relaxation sweeps
+    // append phase timeline (lead thread, %globaltimer ns, accumulated over
+    // appends; pirrt_debug_append_phases): 0 validation, 1 old row lengths,
+    // 2 histogram, 3 scan partials, 4 row offsets, 5 old-delta copy, 6
+    // scatter + init, 7 local relaxation, 8 promising test, 9 appends;
+    // 10, 11 block 0's own time in the P4 chunk copy / the cursor pass
+    unsigned long long app_ns[12];
     alignas(128) int nprom;       // new promising vertices
     alignas(128) int sweep_changed[2];
     // ---- persistent across exploits (zeroed only at create): the state
@@ -139,6 +145,15 @@ struct DevCtl {
     alignas(128) int pre_count[2];
     alignas(128) long long pre_relax[2];
     alignas(128) int pre_tasks[2];
+    // deferred BE-RRT# steps (pirrt_step_async): the current B list as the
+    // last exploit kernel left it (selector, length) and the id of the next
+    // Evaluate -- the state the host mirrors in pirrt_ctx after a synchronous
+    // call, kept here so that a step enqueued behind another one can read it
+    // without a host round trip.  Written by every exploit kernel (lead,
+    // loop_state_out), read by the next step's append and exploit kernels.
+    alignas(128) int dev_Bsel;
+    int dev_Bcount;
+    unsigned dev_ev;
 };
 
 // Everything the persistent exploit kernel touches.
@@ -221,6 +236,12 @@ struct ExploitArgs {
     int* kids;                        // [n]
     int* kids_bsum;                   // [grid blocks] scan partials
     int kids_variant;                 // launch the instantiation that can use the index
+    // deferred step (pirrt_step_async): 0 off; 1 the B list / Evaluate id are
+    // the host's (Bsel, Bcount, ev_base); 2 they are DevCtl's dev_* (a step
+    // enqueued behind another).  In both the step's append has pushed nprom
+    // new members after them, and the kernel returns at once (Alg. 3 guard,
+    // R10) when nprom == 0 or the append was rejected (err != 0)
+    int step_mode;
 };
 
 // ---- goal set (reading R4, goal-set form) ----
@@ -304,6 +325,10 @@ struct AppendArgs {
     long long obase_edges;
     int* Blist;                   // current B list; new promising vertices go to [1+Bcount+k]
     int Bcount;
+    int* chunk_in; int* chunk_out;   // scratch: first row of each old-delta copy chunk
+                                     // (|delta| / kCopyChunk + 2 entries each)
+    int dev_list;                 // 1: the list is Bq[ctl->dev_Bsel] of length ctl->dev_Bcount
+    int* Bq0; int* Bq1;           //    (a deferred step behind another, pirrt_step_async)
     DevCtl* ctl;
     int grid_blocks;
     int per_sm;                   // k_append_fused blocks per SM (append_blocks_per_sm)
@@ -316,6 +341,7 @@ cudaError_t launch_child_count(const int* parent, int v0, int v1, int2* ccd, cud
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
                                 int max_blocks, const L2Window& w, cudaStream_t s);
 constexpr int kAppendMaxBlocks = 2048;
+constexpr int kAppendCopyChunk = 4096;   // old-delta entries per append copy chunk (32 KB of smem destinations)
 int append_blocks_per_sm();
 
 // fold a delta CSR into its base CSR (cost arrays may be NULL: out-index)

@@ -28,6 +28,7 @@ namespace pirrt {
 namespace {
 
 constexpr int kBT = 256;      // block size of the plain kernels
+constexpr int kCopyChunk = kAppendCopyChunk;   // old-delta entries per copy chunk (append P4)
 constexpr int kScanTile = 2048;
 
 inline int grid_for(long long n, int bt = kBT, int cap = 148 * 16) {
@@ -292,6 +293,12 @@ __global__ void k_best_path(const int* parent, const double* g, int n, const int
 // relaxation (R14) or the given policy's edge costs, and the promising test.
 // Grid barriers replace ~20 dependent kernel launches.
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ long long blk_sum_ll(long long x, long long* sm) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
@@ -335,6 +342,13 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     const int lane = threadIdx.x & 31;
     const int gw = tid >> 5, nw = nthreads >> 5;
     long long* cnt0 = a.cnt;
+    unsigned long long t_ph = tid == 0 ? globaltimer_ns() : 0ull;
+#define APP_MARK(k)                                                                \
+    if (tid == 0) {                                                                \
+        const unsigned long long t_ = globaltimer_ns();                            \
+        ctl->app_ns[k] += t_ - t_ph;                                               \
+        t_ph = t_;                                                                 \
+    }
     // promising threshold of the new vertices: the goal cost before the batch
     // (R4; g of old vertices is not written by an append), read once here
     __shared__ double s_thr;
@@ -373,13 +387,28 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         if (err) atomicOr(&ctl->err, err);
     }
     grid.sync();
+    APP_MARK(0);
     if (failed(ctl)) return;                              // uniform: err is final
     // ---- P1 old delta row lengths (both stores)
+    //      and, for the copy in P4, the row holding the first entry of each
+    //      kCopyChunk-entry chunk of the old deltas
     for (int v = tid; v <= n_all; v += nthreads) {
-        cnt0[v] = v < n_old ? a.doff_old[v + 1] - a.doff_old[v] : 0;
-        cnt1[v] = v < n_old ? a.odoff_old[v + 1] - a.odoff_old[v] : 0;
+        long long l0 = 0, l1 = 0;
+        if (v < n_old) {
+            const long long a0 = a.doff_old[v], a1 = a.doff_old[v + 1];
+            const long long b0 = a.odoff_old[v], b1 = a.odoff_old[v + 1];
+            l0 = a1 - a0;
+            l1 = b1 - b0;
+            for (long long k = (a0 + kCopyChunk - 1) / kCopyChunk; k * kCopyChunk < a1; ++k)
+                a.chunk_in[k] = v;
+            for (long long k = (b0 + kCopyChunk - 1) / kCopyChunk; k * kCopyChunk < b1; ++k)
+                a.chunk_out[k] = v;
+        }
+        cnt0[v] = l0;
+        cnt1[v] = l1;
     }
     grid.sync();
+    APP_MARK(1);
     // ---- P2 histogram of the new edges by row
     for (long long e = tid; e < m; e += nthreads) {
         const int sv = a.src[e], dv = a.dst[e];
@@ -391,6 +420,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         }
     }
     grid.sync();
+    APP_MARK(2);
     // ---- P3 exclusive scans -> new delta row offsets (chunk per block)
     const int G = gridDim.x;
     const int chunk = (n_all + G - 1) / G;
@@ -403,6 +433,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         if (threadIdx.x == 0) { bsum[blockIdx.x] = s0; bsum[G + blockIdx.x] = s1; }
     }
     grid.sync();
+    APP_MARK(3);
     {
         long long p0 = 0, p1 = 0, t0 = 0, t1 = 0;
         for (int i = threadIdx.x; i < G; i += kBT) {
@@ -424,30 +455,93 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         if (tid == 0) { a.doff_new[n_all] = t0; a.odoff_new[n_all] = t1; }
     }
     grid.sync();
-    // ---- P4 copy the old delta rows (thread per row), leave cursors; base
-    //      rows of the new vertices are empty
-    for (int v = tid; v < n_all; v += nthreads) {
-        const long long d0 = a.doff_new[v], e0 = a.odoff_new[v];
-        long long len0 = 0, len1 = 0;
-        if (v < n_old) {
-            const long long s0 = a.doff_old[v];
-            len0 = a.doff_old[v + 1] - s0;
-            for (long long k = 0; k < len0; ++k) {
-                a.didx_new[d0 + k] = a.didx_old[s0 + k];
-                a.dcost_new[d0 + k] = a.dcost_old[s0 + k];
+    APP_MARK(4);
+    // ---- P4 copy the old delta rows to their new offsets, scatter cursors
+    //      at their ends; base rows of the new vertices are empty.  The
+    //      copy runs over fixed chunks of old-delta entries (not rows: delta
+    //      rows hold ~6 entries, a thread or warp per row leaves most of each
+    //      transaction unused): a block first writes every entry's
+    //      destination into shared memory, one thread per row the chunk
+    //      touches (from the chunk's first row, marked in P1), then moves
+    //      the chunk with consecutive threads on consecutive entries
+    const unsigned long long t_p4 = tid == 0 ? globaltimer_ns() : 0ull;
+    {
+        __shared__ long long s_dst[kCopyChunk];
+        const long long E0 = a.doff_old[n_old], E1 = a.odoff_old[n_old];
+        const long long nc0 = (E0 + kCopyChunk - 1) / kCopyChunk;
+        const long long nc1 = (E1 + kCopyChunk - 1) / kCopyChunk;
+        for (long long ch = blockIdx.x; ch < nc0 + nc1; ch += gridDim.x) {
+            const bool in = ch < nc0;
+            const long long k = in ? ch : ch - nc0;
+            const long long* off_old = in ? a.doff_old : a.odoff_old;
+            const long long* off_new = in ? a.doff_new : a.odoff_new;
+            const long long c0 = k * kCopyChunk, c1 = min(c0 + kCopyChunk, in ? E0 : E1);
+            // rows [r0, r1]: from the row of the chunk's first entry to the
+            // row of the next chunk's first entry (loads independent of any
+            // test, so a thread's rows are fetched in parallel)
+            const int* crow = in ? a.chunk_in : a.chunk_out;
+            const long long ncs = in ? nc0 : nc1;
+            const int r0 = crow[k];
+            const int r1 = k + 1 < ncs ? crow[k + 1] : n_old - 1;
+#pragma unroll 4
+            for (int r = r0 + (int)threadIdx.x; r <= r1; r += kBT) {
+                const long long o0 = off_old[r], o1 = min(off_old[r + 1], c1);
+                const long long sh = off_new[r] - o0;
+                for (long long e = max(o0, c0); e < o1; ++e) s_dst[e - c0] = e + sh;
             }
-            const long long s1 = a.odoff_old[v];
-            len1 = a.odoff_old[v + 1] - s1;
-            for (long long k = 0; k < len1; ++k) a.odidx_new[e0 + k] = a.odidx_old[s1 + k];
+            __syncthreads();
+            // every thread moves kCopyChunk / kBT entries, U at a time with
+            // all loads issued before the first store (memory-level parallelism)
+            constexpr int U = 8;
+            for (long long g0 = c0; g0 < c1; g0 += U * kBT) {
+                if (in) {
+                    int xi[U];
+                    double xc[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const long long e = g0 + threadIdx.x + j * kBT;
+                        if (e < c1) { xi[j] = __ldcs(&a.didx_old[e]); xc[j] = __ldcs(&a.dcost_old[e]); }
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const long long e = g0 + threadIdx.x + j * kBT;
+                        if (e < c1) {
+                            const long long d = s_dst[e - c0];
+                            a.didx_new[d] = xi[j];
+                            a.dcost_new[d] = xc[j];
+                        }
+                    }
+                } else {
+                    int xi[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const long long e = g0 + threadIdx.x + j * kBT;
+                        if (e < c1) xi[j] = __ldcs(&a.odidx_old[e]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const long long e = g0 + threadIdx.x + j * kBT;
+                        if (e < c1) a.odidx_new[s_dst[e - c0]] = xi[j];
+                    }
+                }
+            }
+            __syncthreads();
         }
-        cnt0[v] = d0 + len0;
-        cnt1[v] = e0 + len1;
     }
+    const unsigned long long t_p4b = tid == 0 ? globaltimer_ns() : 0ull;
+    if (tid == 0) ctl->app_ns[10] += t_p4b - t_p4;
+    for (int v = tid; v < n_all; v += nthreads) {
+        const bool old = v < n_old;
+        cnt0[v] = a.doff_new[v] + (old ? a.doff_old[v + 1] - a.doff_old[v] : 0);
+        cnt1[v] = a.odoff_new[v] + (old ? a.odoff_old[v + 1] - a.odoff_old[v] : 0);
+    }
+    if (tid == 0) ctl->app_ns[11] += globaltimer_ns() - t_p4b;
     for (int v = n_old + 1 + tid; v <= n_all; v += nthreads) {
         a.boff_w[v] = a.base_edges;
         a.oboff_w[v] = a.obase_edges;
     }
     grid.sync();
+    APP_MARK(5);
     // ---- P5 scatter the new edges; init the new vertices
     for (long long e = tid; e < m; e += nthreads) {
         const int sv = a.src[e], dv = a.dst[e];
@@ -472,6 +566,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         a.b[v] = 0;
     }
     grid.sync();
+    APP_MARK(6);
     // ---- P6 policy of the new vertices
     if (a.parent_in) {
         // given policy: pc(v) = cost of the stored edge (parent -> v)
@@ -560,6 +655,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         }
     }
     grid.sync();
+    APP_MARK(7);
     if (failed(ctl)) return;
     // ---- P7 b(v) = g(v) + h(v) < g(x_goal); promising ones join the B list
     // (goal set, R4: the goal cost before the batch)
@@ -585,9 +681,20 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
             pos = __shfl_sync(kFull, pos, leader);
             unsigned lt;
             asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
-            if (p) a.Blist[1 + a.Bcount + pos + __popc(mm & lt)] = v;
+            if (p) {
+                int* bl = a.Blist;
+                int bc = a.Bcount;
+                if (a.dev_list) {                     // written by the previous step's exploit
+                    bl = *(volatile const int*)&ctl->dev_Bsel ? a.Bq1 : a.Bq0;
+                    bc = *(volatile const int*)&ctl->dev_Bcount;
+                }
+                bl[1 + bc + pos + __popc(mm & lt)] = v;
+            }
         }
     }
+    APP_MARK(8);
+    if (tid == 0) ctl->app_ns[9] += 1;
+#undef APP_MARK
 }
 
 }  // namespace

@@ -40,6 +40,7 @@ PIRRT_F_PARENT_FORM = 32
 PIRRT_F_NEIGHBOURS = 64
 PIRRT_F_LOCAL_GROUP = 128
 NCCL_UNIQUE_ID_BYTES = 128
+CUDA_STREAM_LEGACY = 1      # cudaStreamLegacy
 
 # every symbol include/pirrt.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -48,6 +49,7 @@ EXPORTS = (
     "pirrt_get_costs", "pirrt_get_promising", "pirrt_get_parent_costs", "pirrt_get_in_edges", "pirrt_best_path", "pirrt_set_policy", "pirrt_num_vertices",
     "pirrt_num_edges", "pirrt_kernel_launches", "pirrt_last_error", "pirrt_nccl_unique_id", "pirrt_group_exploit",
     "pirrt_set_world", "pirrt_extend_batch", "pirrt_get_points",
+    "pirrt_step_async", "pirrt_step_wait", "pirrt_steps_outstanding",
     # include/pirrt_bench.h (measurement helpers)
     "pirrt_bench_rows", "pirrt_bench_relax", "pirrt_bench_gather", "pirrt_bench_relax_ctx",
 )
@@ -102,6 +104,18 @@ class pirrt_exploit_stats(C.Structure):
     ]
 
 
+class pirrt_step_result(C.Structure):
+    _fields_ = [
+        ("n_new_promising", C.c_int32),
+        ("replanned", C.c_int32),
+        ("path_len", C.c_int64),
+        ("path_cost", C.c_double),
+        ("goal", C.c_int32),
+        ("pad_", C.c_int32),
+        ("stats", pirrt_exploit_stats),
+    ]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `make cuda` "
@@ -120,6 +134,9 @@ def _load():
     lib.pirrt_extend_batch.argtypes = [P, C.c_int32, P, C.c_uint32, P, P]
     lib.pirrt_get_points.argtypes = [P, P, C.c_int64]
     lib.pirrt_exploit_wait.argtypes = [P, C.POINTER(pirrt_exploit_stats)]
+    lib.pirrt_step_async.argtypes = [P, C.c_int32, P, C.c_int64, P, P, P, C.c_uint32]
+    lib.pirrt_step_wait.argtypes = [P, C.POINTER(pirrt_step_result), P, C.c_int64]
+    lib.pirrt_steps_outstanding.argtypes = [P]
     for f in ("pirrt_get_policy", "pirrt_get_costs", "pirrt_get_promising",
               "pirrt_get_parent_costs"):
         getattr(lib, f).argtypes = [P, P, C.c_int64]
@@ -155,6 +172,9 @@ pirrt_set_world = _lib.pirrt_set_world
 pirrt_extend_batch = _lib.pirrt_extend_batch
 pirrt_get_points = _lib.pirrt_get_points
 pirrt_exploit_wait = _lib.pirrt_exploit_wait
+pirrt_step_async = _lib.pirrt_step_async
+pirrt_step_wait = _lib.pirrt_step_wait
+pirrt_steps_outstanding = _lib.pirrt_steps_outstanding
 pirrt_get_policy = _lib.pirrt_get_policy
 pirrt_get_costs = _lib.pirrt_get_costs
 pirrt_get_promising = _lib.pirrt_get_promising
@@ -248,6 +268,17 @@ class ExploitStats:
     pad_: int
 
 
+@dataclass
+class StepResult:
+    """pirrt_step_wait: one deferred BE-RRT# step's result."""
+    n_new_promising: int
+    replanned: bool
+    stats: ExploitStats | None      # None when the Alg. 3 guard skipped the Replan
+    path: np.ndarray
+    cost: float
+    goal: int
+
+
 def _is_torch_cuda(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
 
@@ -311,7 +342,11 @@ class Context:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), NCCL_UNIQUE_ID_BYTES)
             cfg.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p)
         if stream is not None:
-            cfg.stream = int(getattr(stream, "cuda_stream", stream))
+            h = int(getattr(stream, "cuda_stream", stream))
+            # torch's default stream is the legacy NULL stream (handle 0),
+            # which the ABI reads as "create your own": pass cudaStreamLegacy
+            # so that the work is ordered with the caller's default stream
+            cfg.stream = h if h != 0 else CUDA_STREAM_LEGACY
         goal_arr = None
         if goals is not None and len(goals) > 0:
             goal_arr = np.ascontiguousarray(goals, dtype=np.int32)
@@ -418,6 +453,48 @@ class Context:
         st = pirrt_exploit_stats()
         _check(pirrt_exploit_wait(self._h, C.byref(st)))
         return ExploitStats(*(getattr(st, f[0]) for f in pirrt_exploit_stats._fields_))
+
+    def step_async(self, h_new, src, dst, cost, flags=0) -> None:
+        """pirrt_step_async: enqueue append + guarded exploit + best path of one
+        BE-RRT# step and return at once.  numpy arrays (best: pinned, e.g.
+        torch.pin_memory().numpy()) are referenced until the step's
+        step_wait; torch CUDA tensors -> PIRRT_F_DEVICE_PTRS."""
+        if any(_is_torch_cuda(x) for x in (h_new, src, dst, cost)):
+            flags |= PIRRT_F_DEVICE_PTRS
+            m = int(src.numel())
+            _check_device_tensors(int(self.cfg.device), {"dst": m, "cost": m},
+                                  h_new=h_new, src=src, dst=dst, cost=cost)
+            keep = (h_new, src, dst, cost)
+            ptrs = [t.data_ptr() for t in keep]
+            nn = int(h_new.numel())
+        else:
+            keep = (np.ascontiguousarray(h_new, np.float64), np.ascontiguousarray(src, np.int32),
+                    np.ascontiguousarray(dst, np.int32), np.ascontiguousarray(cost, np.float64))
+            ptrs = [a.ctypes.data if a.size else None for a in keep]
+            nn, m = int(keep[0].size), int(keep[1].size)
+        _check(pirrt_step_async(self._h, nn, ptrs[0], m, ptrs[1], ptrs[2], ptrs[3], int(flags)))
+        if not hasattr(self, "_step_keep"):
+            self._step_keep = []
+        self._step_keep.append(keep)        # the library reads them until the step completes
+
+    def step_wait(self) -> StepResult:
+        """pirrt_step_wait: complete the oldest outstanding step."""
+        r = pirrt_step_result()
+        cap = max(self.n, 1)
+        path = np.empty(cap, np.int32)
+        try:
+            _check(pirrt_step_wait(self._h, C.byref(r), path.ctypes.data, cap))
+        finally:
+            if getattr(self, "_step_keep", None):
+                self._step_keep.pop(0)
+        st = ExploitStats(*(getattr(r.stats, f[0]) for f in pirrt_exploit_stats._fields_)) \
+            if r.replanned else None
+        return StepResult(int(r.n_new_promising), bool(r.replanned), st,
+                          path[: r.path_len].copy(), float(r.path_cost), int(r.goal))
+
+    @property
+    def steps_outstanding(self) -> int:
+        return int(pirrt_steps_outstanding(self._h))
 
     def _get(self, fn, dtype):
         n = self.n
