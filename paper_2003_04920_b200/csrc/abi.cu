@@ -231,6 +231,8 @@ struct pirrt_ctx {
                                                              // (-1: 4 n / mean degree; 0: never)
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int* app_chunk = nullptr; int64_t app_chunk_cap = 0;   // append P4 chunk rows (both deltas)
+    unsigned* rdone = nullptr; int64_t rdone_cap = 0;      // append local relaxation stamps
+    unsigned app_id = 0;                                   // appends launched
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
     // goal set G (R4): sorted unique ids incl. x_goal (device copy + host copy)
     int* goals = nullptr; int64_t goals_cap = 0;
@@ -411,6 +413,13 @@ int ensure_vertices(pirrt_ctx* c, int64_t need) {
         c->q_cap = qc;
     }
     if ((rc = grow(c->path, c->path_cap, cap + 8, 0, s))) return rc;
+    {
+        // stamps of the local relaxation: only this append's new vertices are
+        // read, and their ids were never stamped with a later id -- zeroed once
+        const int64_t before = c->rdone_cap;
+        if ((rc = grow(c->rdone, c->rdone_cap, cap, 0, s))) return rc;
+        if (c->rdone_cap != before) CU(cudaMemsetAsync(c->rdone, 0, (size_t)c->rdone_cap * sizeof(unsigned), s));
+    }
     c->vcap = cap;
     return 0;
 }
@@ -429,6 +438,7 @@ void free_all(pirrt_ctx* c) {
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
     if (c->app_chunk) cudaFree(c->app_chunk);
+    if (c->rdone) cudaFree(c->rdone);
     for (auto& sl : c->slot) {
         if (sl.ctl) cudaFreeHost(sl.ctl);
         if (sl.head) cudaFreeHost(sl.head);
@@ -549,6 +559,8 @@ void fill_append_args(pirrt_ctx* c, AppendArgs& a, int nb, int n_old, int n_new,
     a.obase_edges = c->obase_edges;
     a.Blist = c->Bq[c->Bsel]; a.Bcount = c->Bcount;
     a.Bq0 = c->Bq[0]; a.Bq1 = c->Bq[1];
+    a.rdone = c->rdone;
+    a.app_id = ++c->app_id;
     const int64_t nch = c->delta_edges / kAppendCopyChunk + 2;
     a.chunk_in = c->app_chunk; a.chunk_out = c->app_chunk + nch;
     a.cnt = c->cnt; a.scan_tmp = c->scan_tmp;

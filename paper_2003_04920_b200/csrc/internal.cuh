@@ -117,7 +117,7 @@ struct DevCtl {
     // appends; pirrt_debug_append_phases): 0 validation, 1 old row lengths,
     // 2 histogram, 3 scan partials, 4 row offsets, 5 old-delta copy, 6
     // scatter + init, 7 local relaxation, 8 promising test, 9 appends;
-    // 10, 11 block 0's own time in the P4 chunk copy / the cursor pass
+    // 10 block 0's own time in the P4 chunk copy, 11 unused
     unsigned long long app_ns[12];
     alignas(128) int nprom;       // new promising vertices
     alignas(128) int sweep_changed[2];
@@ -325,6 +325,8 @@ struct AppendArgs {
     long long obase_edges;
     int* Blist;                   // current B list; new promising vertices go to [1+Bcount+k]
     int Bcount;
+    unsigned* rdone;              // local relaxation: rdone[v] == app_id once v is final
+    unsigned app_id;              // this append's id (> every earlier one)
     int* chunk_in; int* chunk_out;   // scratch: first row of each old-delta copy chunk
                                      // (|delta| / kCopyChunk + 2 entries each)
     int dev_list;                 // 1: the list is Bq[ctl->dev_Bsel] of length ctl->dev_Bcount
@@ -341,7 +343,7 @@ cudaError_t launch_child_count(const int* parent, int v0, int v1, int2* ccd, cud
 cudaError_t launch_append_fused(const AppendArgs& a, long long* cnt1, long long* bsum,
                                 int max_blocks, const L2Window& w, cudaStream_t s);
 constexpr int kAppendMaxBlocks = 2048;
-constexpr int kAppendCopyChunk = 4096;   // old-delta entries per append copy chunk (32 KB of smem destinations)
+constexpr int kAppendCopyChunk = 2048;   // old-delta entries per append copy chunk (16 KB of smem destinations)
 int append_blocks_per_sm();
 
 // fold a delta CSR into its base CSR (cost arrays may be NULL: out-index)

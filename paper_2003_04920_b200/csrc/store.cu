@@ -293,6 +293,16 @@ __global__ void k_best_path(const int* parent, const double* g, int n, const int
 // relaxation (R14) or the given policy's edge costs, and the promising test.
 // Grid barriers replace ~20 dependent kernel launches.
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -392,6 +402,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     // ---- P1 old delta row lengths (both stores)
     //      and, for the copy in P4, the row holding the first entry of each
     //      kCopyChunk-entry chunk of the old deltas
+#pragma unroll 4
     for (int v = tid; v <= n_all; v += nthreads) {
         long long l0 = 0, l1 = 0;
         if (v < n_old) {
@@ -443,21 +454,42 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         }
         p0 = blk_sum_ll(p0, sm); p1 = blk_sum_ll(p1, sm);
         t0 = blk_sum_ll(t0, sm); t1 = blk_sum_ll(t1, sm);
-        for (int base = c0; base < c1; base += kBT) {
-            const int v = base + threadIdx.x;
-            const long long x0 = v < c1 ? cnt0[v] : 0, x1 = v < c1 ? cnt1[v] : 0;
-            long long tot0, tot1;
-            const long long o0 = blk_excl_scan_ll(x0, sm, &tot0);
-            const long long o1 = blk_excl_scan_ll(x1, sm, &tot1);
-            if (v < c1) { a.doff_new[v] = p0 + o0; a.odoff_new[v] = p1 + o1; }
-            p0 += tot0; p1 += tot1;
+        // warp-contiguous sub-ranges of the block's chunk, lanes on
+        // consecutive rows (coalesced): pass 1 the warps' sums, pass 2 a
+        // warp scan per 32 rows carried along the sub-range
+        constexpr int W = kBT / 32;
+        const int wl = threadIdx.x >> 5;
+        const int wc = ((chunk + W - 1) / W + 31) & ~31;
+        const int w0 = min(c1, c0 + wl * wc), w1 = min(c1, w0 + wc);
+        __shared__ long long s_w[2][W];
+        long long q0 = 0, q1 = 0;
+#pragma unroll 4
+        for (int v = w0 + lane; v < w1; v += 32) { q0 += cnt0[v]; q1 += cnt1[v]; }
+        for (int o = 16; o; o >>= 1) {
+            q0 += __shfl_xor_sync(kFull, q0, o);
+            q1 += __shfl_xor_sync(kFull, q1, o);
+        }
+        if (lane == 0) { s_w[0][wl] = q0; s_w[1][wl] = q1; }
+        __syncthreads();
+        for (int i = 0; i < wl; ++i) { p0 += s_w[0][i]; p1 += s_w[1][i]; }
+        for (int base = w0; base < w1; base += 32) {
+            const int v = base + lane;
+            const long long x0 = v < w1 ? cnt0[v] : 0, x1 = v < w1 ? cnt1[v] : 0;
+            long long i0 = x0, i1 = x1;
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y0 = __shfl_up_sync(kFull, i0, o), y1 = __shfl_up_sync(kFull, i1, o);
+                if (lane >= o) { i0 += y0; i1 += y1; }
+            }
+            if (v < w1) { a.doff_new[v] = p0 + i0 - x0; a.odoff_new[v] = p1 + i1 - x1; }
+            p0 += __shfl_sync(kFull, i0, 31);
+            p1 += __shfl_sync(kFull, i1, 31);
         }
         if (tid == 0) { a.doff_new[n_all] = t0; a.odoff_new[n_all] = t1; }
     }
     grid.sync();
     APP_MARK(4);
-    // ---- P4 copy the old delta rows to their new offsets, scatter cursors
-    //      at their ends; base rows of the new vertices are empty.  The
+    // ---- P4 copy the old delta rows to their new offsets (each at the
+    //      start of its row); base rows of the new vertices are empty.  The
     //      copy runs over fixed chunks of old-delta entries (not rows: delta
     //      rows hold ~6 entries, a thread or warp per row leaves most of each
     //      transaction unused): a block first writes every entry's
@@ -492,7 +524,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
             __syncthreads();
             // every thread moves kCopyChunk / kBT entries, U at a time with
             // all loads issued before the first store (memory-level parallelism)
-            constexpr int U = 8;
+            constexpr int U = 4;
             for (long long g0 = c0; g0 < c1; g0 += U * kBT) {
                 if (in) {
                     int xi[U];
@@ -528,14 +560,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
             __syncthreads();
         }
     }
-    const unsigned long long t_p4b = tid == 0 ? globaltimer_ns() : 0ull;
-    if (tid == 0) ctl->app_ns[10] += t_p4b - t_p4;
-    for (int v = tid; v < n_all; v += nthreads) {
-        const bool old = v < n_old;
-        cnt0[v] = a.doff_new[v] + (old ? a.doff_old[v + 1] - a.doff_old[v] : 0);
-        cnt1[v] = a.odoff_new[v] + (old ? a.odoff_old[v + 1] - a.odoff_old[v] : 0);
-    }
-    if (tid == 0) ctl->app_ns[11] += globaltimer_ns() - t_p4b;
+    if (tid == 0) ctl->app_ns[10] += globaltimer_ns() - t_p4;
     for (int v = n_old + 1 + tid; v <= n_all; v += nthreads) {
         a.boff_w[v] = a.base_edges;
         a.oboff_w[v] = a.obase_edges;
@@ -543,17 +568,19 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     grid.sync();
     APP_MARK(5);
     // ---- P5 scatter the new edges; init the new vertices
+    //      (cnt still holds each row's new length, old + new entries: the
+    //      new ones fill the row from its end, behind the copied old ones)
     for (long long e = tid; e < m; e += nthreads) {
         const int sv = a.src[e], dv = a.dst[e];
         const double c = a.cost[e] + 0.0;                // -0.0 -> +0.0 (R12)
-        long long p = (long long)atomicAdd((unsigned long long*)&cnt0[dv], 1ull);
+        long long p = a.doff_new[dv] + (long long)atomicAdd((unsigned long long*)&cnt0[dv], ~0ull) - 1;
         a.didx_new[p] = sv; a.dcost_new[p] = c;
-        p = (long long)atomicAdd((unsigned long long*)&cnt1[sv], 1ull);
+        p = a.odoff_new[sv] + (long long)atomicAdd((unsigned long long*)&cnt1[sv], ~0ull) - 1;
         a.odidx_new[p] = dv;
         if (a.undirected) {
-            p = (long long)atomicAdd((unsigned long long*)&cnt0[sv], 1ull);
+            p = a.doff_new[sv] + (long long)atomicAdd((unsigned long long*)&cnt0[sv], ~0ull) - 1;
             a.didx_new[p] = dv; a.dcost_new[p] = c;
-            p = (long long)atomicAdd((unsigned long long*)&cnt1[dv], 1ull);
+            p = a.odoff_new[dv] + (long long)atomicAdd((unsigned long long*)&cnt1[dv], ~0ull) - 1;
             a.odidx_new[p] = sv;
         }
     }
@@ -594,65 +621,58 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
             }
         }
     } else if (n_new > 0) {
-        // Extend's local relaxation (R14): chaotic in-place sweeps
-        // over the new vertices until a full sweep changes no (g, parent) pair;
-        // every dependency goes from a lower to a higher id, so the fixed point
-        // is unique and equals the sequential id-order result bit for bit.
-        const bool lead = tid == 0;
-        for (int sw = 0;; ++sw) {
-            int* chg = &ctl->sweep_changed[sw & 1];
-            if (lead) ctl->sweep_changed[(sw + 1) & 1] = 0;
-            bool my_change = false;
-            for (int i = gw; i < n_new; i += nw) {
-                const int v = n_old + i;
-                double best = INFINITY;
-                int arg = INT_MAX;
-                double argc = 0.0;
-                for (long long k = a.boff[v] + lane; k < a.boff[v + 1]; k += 32) {
-                    const int u = a.bidx[k];
-                    if (u >= v) continue;
-                    const double c = a.bcost[k];
-                    const double cand = *(volatile const double*)&a.g[u] + c;
-                    if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
-                }
-                for (long long k = a.doff_new[v] + lane; k < a.doff_new[v + 1]; k += 32) {
-                    const int u = a.didx_new[k];
-                    if (u >= v) continue;
-                    const double c = a.dcost_new[k];
-                    const double cand = *(volatile const double*)&a.g[u] + c;
-                    if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
-                }
-                double wb = best;
-                int wa = arg;
-                for (int o = 16; o; o >>= 1) {
-                    const double ob = __shfl_xor_sync(kFull, wb, o);
-                    const int oa = __shfl_xor_sync(kFull, wa, o);
-                    if (ob < wb || (ob == wb && oa < wa)) { wb = ob; wa = oa; }
-                }
-                const unsigned mm = __ballot_sync(kFull, best == wb && arg == wa);
-                const double c = __shfl_sync(kFull, argc, __ffs(mm) - 1);
-                if (lane == 0) {
-                    int np;
-                    double ng, npc;
-                    if (wb < INFINITY) { np = wa; ng = wb; npc = c; }
-                    else { np = -1; ng = INFINITY; npc = 0.0; }
-                    if (np != a.parent[v] || __double_as_longlong(ng) != __double_as_longlong(*(volatile double*)&a.g[v])) {
-                        *(volatile double*)&a.g[v] = ng;
-                        a.parent[v] = np;
-                        a.pc[v] = npc;
-                        my_change = true;
-                    }
-                }
+        // Extend's local relaxation (R14) in ONE dataflow pass:
+        // in increasing id order g(v) = min over in-edges (u -> v), u < v,
+        // of g(u) + c (lowest u on ties).  A warp takes new vertices in
+        // increasing id order; where an in-neighbour u is itself new, the
+        // lane waits until u is final (rdone[u] == this append's id, stored
+        // with release after u's g / parent / pc).  Every dependency points
+        // to a lower id and all warps are co-resident (cooperative launch),
+        // so the lowest unfinished vertex can always proceed: the result is
+        // the sequential id-order result bit for bit, without the grid-wide
+        // sweeps of a Jacobi relaxation.
+        const unsigned aid = a.app_id;
+        for (int i = gw; i < n_new; i += nw) {
+            const int v = n_old + i;
+            double best = INFINITY;
+            int arg = INT_MAX;
+            double argc = 0.0;
+            for (long long k = a.boff[v] + lane; k < a.boff[v + 1]; k += 32) {
+                const int u = a.bidx[k];
+                if (u >= v) continue;
+                if (u >= n_old) while (ld_acquire_u32(&a.rdone[u]) != aid) {}
+                const double c = a.bcost[k];
+                const double cand = *(volatile const double*)&a.g[u] + c;
+                if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
             }
-            // one flag update per block, and none once some block has set it
-            if (__syncthreads_or(my_change) && threadIdx.x == 0 && *(volatile int*)chg == 0)
-                atomicOr(chg, 1);
-            grid.sync();
-            const int any = *(volatile int*)chg;
-            if (lead) ctl->sweeps = sw + 1;
-            if (!any) break;
-            grid.sync();   // everyone has read chg before it is reset two sweeps later
+            for (long long k = a.doff_new[v] + lane; k < a.doff_new[v + 1]; k += 32) {
+                const int u = a.didx_new[k];
+                if (u >= v) continue;
+                if (u >= n_old) while (ld_acquire_u32(&a.rdone[u]) != aid) {}
+                const double c = a.dcost_new[k];
+                const double cand = *(volatile const double*)&a.g[u] + c;
+                if (cand < best || (cand == best && u < arg)) { best = cand; arg = u; argc = c; }
+            }
+            double wb = best;
+            int wa = arg;
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, wb, o);
+                const int oa = __shfl_xor_sync(kFull, wa, o);
+                if (ob < wb || (ob == wb && oa < wa)) { wb = ob; wa = oa; }
+            }
+            const unsigned mm = __ballot_sync(kFull, best == wb && arg == wa);
+            const double c = __shfl_sync(kFull, argc, __ffs(mm) - 1);
+            if (lane == 0) {
+                if (wb < INFINITY) {
+                    *(volatile double*)&a.g[v] = wb;
+                    a.parent[v] = wa;
+                    a.pc[v] = c;
+                }                                          // (else: -1 / +inf / 0 from P5)
+                st_release_u32(&a.rdone[v], aid);
+            }
+            __syncwarp();
         }
+        if (tid == 0) ctl->sweeps = 1;
     }
     grid.sync();
     APP_MARK(7);
