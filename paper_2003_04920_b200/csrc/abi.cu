@@ -232,6 +232,7 @@ struct pirrt_ctx {
     long long* app_bsum = nullptr; int64_t app_bsum_cap = 0;
     int* app_chunk = nullptr; int64_t app_chunk_cap = 0;   // append P4 chunk rows (both deltas)
     unsigned* rdone = nullptr; int64_t rdone_cap = 0;      // append local relaxation stamps
+    int* fold_mark = nullptr; int64_t fold_mark_cap = 0;   // fold: chunk rows of base + delta
     unsigned app_id = 0;                                   // appends launched
     int64_t launches = 0;         // kernels launched (diagnostics, bench gpu_launches)
     // goal set G (R4): sorted unique ids incl. x_goal (device copy + host copy)
@@ -439,6 +440,7 @@ void free_all(pirrt_ctx* c) {
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
     if (c->app_chunk) cudaFree(c->app_chunk);
     if (c->rdone) cudaFree(c->rdone);
+    if (c->fold_mark) cudaFree(c->fold_mark);
     for (auto& sl : c->slot) {
         if (sl.ctl) cudaFreeHost(sl.ctl);
         if (sl.head) cudaFreeHost(sl.head);
@@ -494,6 +496,13 @@ int fold(pirrt_ctx* c, long long*& boff, int64_t& boff_cap, int*& bidx, int64_t&
     a.doff = doff; a.didx = didx; a.dcost = dcost;
     a.boff_new = sboff; a.bidx_new = sbidx; a.bcost_new = bcost ? sbcost : nullptr;
     a.cnt = c->cnt; a.scan_tmp = c->scan_tmp; a.n = c->n;
+    // the base holds boff[n] entries (this rank's rows on a partitioned
+    // store), the delta E - base_edges; chunk marks for the merge
+    a.Eb = bcost ? c->base_edges : c->obase_edges;
+    a.Ed = E - a.Eb;
+    const int64_t nA = a.Eb / kAppendCopyChunk + 2, nB = a.Ed / kAppendCopyChunk + 2;
+    if ((rc = grow(c->fold_mark, c->fold_mark_cap, nA + nB, 0, c->stream))) return rc;
+    a.markA = c->fold_mark; a.markB = c->fold_mark + nA;
     a.own_n = partition ? c->own_n : 0;
     a.own_r = c->own_r;
     const long long l0 = g_kernel_launches;

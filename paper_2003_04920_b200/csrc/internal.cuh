@@ -352,6 +352,9 @@ struct CompactArgs {
     const long long* doff; const int* didx; const double* dcost;
     long long* boff_new; int* bidx_new; double* bcost_new;
     long long* cnt; long long* scan_tmp;
+    int* markA; int* markB;       // scratch: first row of each kAppendCopyChunk-entry chunk of
+                                  // the base / the delta (Eb / C + 2, Ed / C + 2 entries)
+    long long Eb, Ed;             // entries of the base / the delta
     int n;
     int own_n, own_r;             // partitioned store (sharded, P > 1): keep only the rows of
                                   // v with v % own_n == own_r (own_n = 0: every row)

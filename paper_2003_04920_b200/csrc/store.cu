@@ -178,33 +178,71 @@ __device__ __forceinline__ bool row_kept(int v, int own_n, int own_r) {
     return own_n <= 1 || v % own_n == own_r;
 }
 
-__global__ void k_base_count(const long long* boff, const long long* doff, int n, long long* cnt,
-                             int own_n, int own_r) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        cnt[v] = row_kept(v, own_n, own_r) ? (boff[v + 1] - boff[v]) + (doff[v + 1] - doff[v]) : 0;
+// row lengths of the merged store, and the first row of every
+// kCopyChunk-entry chunk of the base and of the delta (k_base_merge)
+__global__ void k_base_count(CompactArgs a) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += gridDim.x * blockDim.x) {
+        const long long b0 = a.boff[v], b1 = a.boff[v + 1], d0 = a.doff[v], d1 = a.doff[v + 1];
+        a.cnt[v] = row_kept(v, a.own_n, a.own_r) ? (b1 - b0) + (d1 - d0) : 0;
+        for (long long k = (b0 + kCopyChunk - 1) / kCopyChunk; k * kCopyChunk < b1; ++k) a.markA[k] = v;
+        for (long long k = (d0 + kCopyChunk - 1) / kCopyChunk; k * kCopyChunk < d1; ++k) a.markB[k] = v;
+    }
 }
 
-__global__ void k_base_merge(const long long* boff, const int* bidx, const double* bcost,
-                             const long long* doff, const int* didx, const double* dcost,
-                             const long long* boff_new, int* bidx_new, double* bcost_new, int n,
-                             int own_n, int own_r) {
-    const int lane = threadIdx.x & 31;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int v = w; v < n; v += nw) {
-        if (!row_kept(v, own_n, own_r)) continue;         // (warp-uniform)
-        long long o = boff_new[v];
-        const long long b0 = boff[v], bl = boff[v + 1] - b0;
-        for (long long k = lane; k < bl; k += 32) {
-            bidx_new[o + k] = bidx[b0 + k];
-            if (bcost_new) bcost_new[o + k] = bcost[b0 + k];
+// The fold's move: row v of the new base = base row v, then delta row v.
+// As the append's old-delta copy (P4): fixed chunks of source entries, the
+// destinations of a chunk written to shared memory one thread per row, then
+// the entries moved with consecutive threads on consecutive entries (a warp
+// per row used ~60 of every 128 lanes' worth of a base row and stalled on
+// the row bounds).  Rows not kept (partitioned store) are skipped.
+__global__ void __launch_bounds__(kBT) k_base_merge(CompactArgs a) {
+    __shared__ long long s_dst[kCopyChunk];
+    const long long ncA = (a.Eb + kCopyChunk - 1) / kCopyChunk;
+    const long long ncB = (a.Ed + kCopyChunk - 1) / kCopyChunk;
+    for (long long ch = blockIdx.x; ch < ncA + ncB; ch += gridDim.x) {
+        const bool A = ch < ncA;
+        const long long k = A ? ch : ch - ncA;
+        const long long* off = A ? a.boff : a.doff;
+        const int* mark = A ? a.markA : a.markB;
+        const long long c0 = k * kCopyChunk, c1 = min(c0 + kCopyChunk, A ? a.Eb : a.Ed);
+        const int r0 = mark[k];
+        const int r1 = k + 1 < (A ? ncA : ncB) ? mark[k + 1] : a.n - 1;
+#pragma unroll 4
+        for (int r = r0 + (int)threadIdx.x; r <= r1; r += kBT) {
+            const long long o0 = off[r], o1 = min(off[r + 1], c1);
+            long long base = a.boff_new[r];
+            if (!A) base += a.boff[r + 1] - a.boff[r];
+            const bool keep = row_kept(r, a.own_n, a.own_r);
+            for (long long e = max(o0, c0); e < o1; ++e) s_dst[e - c0] = keep ? base + (e - o0) : -1;
         }
-        o += bl;
-        const long long d0 = doff[v], dl = doff[v + 1] - d0;
-        for (long long k = lane; k < dl; k += 32) {
-            bidx_new[o + k] = didx[d0 + k];
-            if (bcost_new) bcost_new[o + k] = dcost[d0 + k];
+        __syncthreads();
+        const int* sidx = A ? a.bidx : a.didx;
+        const double* scost = A ? a.bcost : a.dcost;
+        constexpr int U = 4;
+        for (long long g0 = c0; g0 < c1; g0 += U * kBT) {
+            int xi[U];
+            double xc[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const long long e = g0 + threadIdx.x + j * kBT;
+                if (e < c1) {
+                    xi[j] = __ldcs(&sidx[e]);
+                    if (a.bcost_new) xc[j] = __ldcs(&scost[e]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const long long e = g0 + threadIdx.x + j * kBT;
+                if (e < c1) {
+                    const long long d = s_dst[e - c0];
+                    if (d >= 0) {
+                        a.bidx_new[d] = xi[j];
+                        if (a.bcost_new) a.bcost_new[d] = xc[j];
+                    }
+                }
+            }
         }
+        __syncthreads();
     }
 }
 
@@ -807,12 +845,11 @@ int append_blocks_per_sm() {
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
     cudaError_t e;
     ++g_kernel_launches;
-    k_base_count<<<grid_for(a.n), kBT, 0, s>>>(a.boff, a.doff, a.n, a.cnt, a.own_n, a.own_r);
+    k_base_count<<<grid_for(a.n), kBT, 0, s>>>(a);
     if ((e = scan_exclusive(a.cnt, a.boff_new, a.n, a.scan_tmp, s)) != cudaSuccess) return e;
     ++g_kernel_launches;
-    k_base_merge<<<grid_for((long long)a.n * 32), kBT, 0, s>>>(
-        a.boff, a.bidx, a.bcost, a.doff, a.didx, a.dcost, a.boff_new, a.bidx_new, a.bcost_new, a.n,
-        a.own_n, a.own_r);
+    const long long chunks = (a.Eb + kCopyChunk - 1) / kCopyChunk + (a.Ed + kCopyChunk - 1) / kCopyChunk;
+    k_base_merge<<<grid_for(chunks, 1), kBT, 0, s>>>(a);
     return cudaGetLastError();
 }
 
