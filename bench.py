@@ -391,26 +391,38 @@ def run_cuda(a, dev):
     while ctx.steps_outstanding:
         ctx.step_wait()
     torch.cuda.synchronize()
+    e2e_ex = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
     e0.record(stream)
     for i in range(W2, W2 + a.steps):
+        pev[i - W2][0].record(stream)
         ctx.step_async(*rest[i], flags=EDGES_UNDIRECTED)
+        pev[i - W2][1].record(stream)
         h2d += sum(x.nbytes for x in rest[i])
         if ctx.steps_outstanding >= depth:
             r = ctx.step_wait()
             d2h += 4 + r.path.nbytes + 16 + st_bytes
+            if r.replanned:
+                e2e_ex.append(r.stats.device_ms)
     while ctx.steps_outstanding:
         r = ctx.step_wait()
         d2h += 4 + r.path.nbytes + 16 + st_bytes
+        if r.replanned:
+            e2e_ex.append(r.stats.device_ms)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_pipe_ms = e0.elapsed_time(e1)
+    e2e_dev_ms = sum(x.elapsed_time(y) for x, y in pev)   # the steps' own stream spans
     clk = clocks.stop()
     ex = [s for s in stats if s is not None]
     res = {
         "step_ms": step_ms, "launches": launches, "ex": ex, "n_exploits": len(ex),
         "relax_per_step": [s.relaxations if s else 0 for s in stats],
         "e2e_ms": float(e2e_pipe_ms), "e2e_sync_ms": float(sum(e2e_ms)),
+        "e2e_dev_ms": float(e2e_dev_ms),
+        "e2e_exploit_ms": float(statistics.mean(e2e_ex)) if e2e_ex else 0.0,
         "e2e_sync_steps": len(e2e_ms), "h2d": h2d / a.steps, "d2h": d2h / a.steps,
         "clocks": clk, "t_gen": t_gen, "t_pre": t_pre,
         "graph": {"n_total": g.n, "pairs": g.n_pairs, "mean_degree": g.mean_degree,
@@ -688,7 +700,9 @@ def main_cuda_single(a):
                         "H2D of batch k+1 from pinned host memory overlaps the exploit of batch "
                         "k); per step one best path + stats read-back",
                 "sync_mode": "one synchronous call after another (append, exploit, best_path)",
-                "sync_value": round(res["e2e_sync_ms"] / max(1, res["e2e_sync_steps"]), 4)},
+                "sync_value": round(res["e2e_sync_ms"] / max(1, res["e2e_sync_steps"]), 4),
+                "stream_ms_per_step": round(res["e2e_dev_ms"] / a.steps, 4),
+                "exploit_ms_mean": round(res["e2e_exploit_ms"], 4)},
         "gpu_launches": int(res["launches"]),
         "clocks": res["clocks"],
         "setup_s": {"generate": round(res["t_gen"], 2), "preload_replay": round(res["t_pre"], 2)},

@@ -63,6 +63,7 @@ struct IterCtl {
     alignas(128) int acount;
     alignas(128) long long relax_work;
     alignas(128) int tasks_work;
+    alignas(128) int wide_next;                // improve_wide_kernel: next unclaimed task
 };
 
 // One Improve result in sharded mode (all-gathered between ranks).
