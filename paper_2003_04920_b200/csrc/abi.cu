@@ -570,6 +570,15 @@ void fill_append_args(pirrt_ctx* c, AppendArgs& a, int nb, int n_old, int n_new,
     a.Bq0 = c->Bq[0]; a.Bq1 = c->Bq[1];
     a.rdone = c->rdone;
     a.app_id = ++c->app_id;
+    // P8: prebuild the next exploit's first Improve (single GPU, the
+    // incremental Improve's own preconditions; a VALIDATE append may still be
+    // rejected after the kernel, a given policy forces a full Improve)
+    a.pre_ok = (!c->sharded && c->inc_imp > 0 && !validate && !d_parent &&
+                !(c->cfg.flags & (PIRRT_F_PRUNE_OFF | PIRRT_F_NEIGHBOURS))) ? 1 : 0;
+    a.inc_max = (int)std::min<int64_t>(c->inc_max, c->dcap - 64);
+    a.inc_imp = c->inc_imp;
+    a.istamp = c->istamp; a.alist = c->alist; a.acap = (int)c->g_cap;
+    a.dirty = c->dirty; a.gcl = c->gcl; a.dcap = (int)c->dcap;
     const int64_t nch = c->delta_edges / kAppendCopyChunk + 2;
     a.chunk_in = c->app_chunk; a.chunk_out = c->app_chunk + nch;
     a.cnt = c->cnt; a.scan_tmp = c->scan_tmp;

@@ -118,7 +118,7 @@ struct DevCtl {
     // appends; pirrt_debug_append_phases): 0 validation, 1 old row lengths,
     // 2 histogram, 3 scan partials, 4 row offsets, 5 old-delta copy, 6
     // scatter + init, 7 local relaxation, 8 promising test, 9 appends;
-    // 10 block 0's own time in the P4 chunk copy, 11 unused
+    // 10 block 0's own time in the P4 chunk copy, 11 the prebuild (P8)
     unsigned long long app_ns[12];
     alignas(128) int nprom;       // new promising vertices
     alignas(128) int sweep_changed[2];
@@ -155,6 +155,9 @@ struct DevCtl {
     alignas(128) int dev_Bsel;
     int dev_Bcount;
     unsigned dev_ev;
+    // the append prebuilt the task list (and counters) of Improve app_pre_k
+    // (0: none), slot app_pre_k & 1 of alist / pre_count / pre_relax / pre_tasks
+    unsigned app_pre_k;
 };
 
 // Everything the persistent exploit kernel touches.
@@ -326,6 +329,12 @@ struct AppendArgs {
     long long obase_edges;
     int* Blist;                   // current B list; new promising vertices go to [1+Bcount+k]
     int Bcount;
+    // P8: the next exploit's first Improve prebuilt (pre_ok: single GPU, no
+    // PRUNE_OFF / NEIGHBOURS / VALIDATE / given policy, incremental Improve on)
+    int pre_ok;
+    int inc_max, inc_imp;
+    unsigned* istamp; int* alist; int acap;
+    const int* dirty; const int* gcl; int dcap;
     unsigned* rdone;              // local relaxation: rdone[v] == app_id once v is final
     unsigned app_id;              // this append's id (> every earlier one)
     int* chunk_in; int* chunk_out;   // scratch: first row of each old-delta copy chunk

@@ -378,6 +378,153 @@ __device__ __forceinline__ long long blk_excl_scan_ll(long long x, long long* sm
     return before + inc - x;
 }
 
+// ---- P8 of the append: the next exploit's first Improve, prebuilt.
+// The incremental Improve scans only the members of I
+// whose result can differ from the previous Improve's: (a) its commits,
+// (b) vertices whose g an Evaluate changed since, and their out-neighbours,
+// (c) members that joined I since, (d) out-neighbours of the vertices
+// appended since, (e) the goals.  Between exploits (c) and (d) come from
+// appends only, so the append lists them here -- from this batch's own edge
+// list (thread per edge: a new vertex's out-neighbours are the heads of its
+// new edges) -- and the exploit's first Improve takes the list as prebuilt
+// (no discovery phase, no grid barrier).  The first append after an Improve
+// also lists (a), (b), (e) and whatever earlier appends added (exactly the
+// exploit's own discovery); later appends continue the list (stamps 2k:
+// below the 2k + 1 of a discovery of the same Improve, which runs whenever
+// the list is not valid).  The full Improve's counters over I (Sum of
+// in-degrees, |I|: the paper's relaxation count) are recomputed by every
+// append, since new in-edges change the members' in-degrees.  Valid under the
+// incremental Improve's own conditions (evaluated here on the same device
+// state); app_pre_k = k marks it valid.
+__device__ __forceinline__ bool app_in_I(const AppendArgs& a, int v) {
+    return v != kRoot && (a.b[v] || is_goal(a.goals, a.n_goals, v));
+}
+
+__device__ __forceinline__ long long app_in_degree(const AppendArgs& a, int v) {
+    return (a.boff[v + 1] - a.boff[v]) + (a.doff_new[v + 1] - a.doff_new[v]);
+}
+
+__device__ __forceinline__ void app_list_push(int* buf, int* cnt, bool want, int v) {
+    const unsigned m = __ballot_sync(kFull, want);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(cnt, __popc(m));
+    base = __shfl_sync(kFull, base, leader);
+    unsigned lt;
+    asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
+    if (want) buf[base + __popc(m & lt)] = v;
+}
+
+__device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int tid, int nthreads,
+                                long long* sm) {
+    DevCtl* ctl = a.ctl;
+    const int lane = threadIdx.x & 31;
+    const int gwarp = tid >> 5, nwarps = nthreads >> 5;
+    const int n_old = a.n_old, n_all = a.n_old + a.n_new;
+    const int* bl = a.Blist;
+    int bc = a.Bcount;
+    if (a.dev_list) {
+        bl = *(volatile const int*)&ctl->dev_Bsel ? a.Bq1 : a.Bq0;
+        bc = *(volatile const int*)&ctl->dev_Bcount;
+    }
+    const int Bc = bc + *(volatile const int*)&ctl->nprom;
+    const int imp_full = *(volatile const int*)&ctl->imp_full;
+    const int gc_n = *(volatile const int*)&ctl->gc_count[(k - 1) & 1];
+    const int c_n = *(volatile const int*)&ctl->c_n, c_buf = *(volatile const int*)&ctl->c_buf;
+    const int L_imp = *(volatile const int*)&ctl->L_imp, n_imp = *(volatile const int*)&ctl->n_imp;
+    const int live = Bc - *(volatile const int*)&ctl->holes;
+    const bool ok = !imp_full && gc_n < a.inc_max && c_n < a.inc_max && L_imp <= Bc && n_imp <= n_all &&
+                    Bc - L_imp <= a.inc_max &&
+                    (a.inc_imp > 1 || 4LL * (gc_n + (n_all - n_imp)) < (long long)live);
+    if (!ok) {
+        if (tid == 0) ctl->app_pre_k = 0;
+        return;
+    }
+    int* tl = a.alist + (size_t)(k & 1u) * a.acap;
+    int* tc = &ctl->pre_count[k & 1];
+    const unsigned ks = 2u * k;
+    // the full Improve's counters over I (every member of the list, every
+    // existing goal)
+    long long rx = 0, tk = 0;
+    for (int t = tid; t < Bc; t += nthreads) {
+        const int v = bl[1 + t];
+        if (v < 0 || is_goal(a.goals, a.n_goals, v)) continue;
+        rx += app_in_degree(a, v);
+        ++tk;
+    }
+    for (int t = tid; t < a.n_goals; t += nthreads) {
+        const int v = a.goals[t];
+        if (v >= n_all) continue;
+        rx += app_in_degree(a, v);
+        ++tk;
+    }
+    rx = blk_sum_ll(rx, sm);
+    tk = blk_sum_ll(tk, sm);
+    if (threadIdx.x == 0) {
+        if (rx) atomicAdd((unsigned long long*)&ctl->pre_relax[k & 1], (unsigned long long)rx);
+        if (tk) atomicAdd(&ctl->pre_tasks[k & 1], (int)tk);
+    }
+    // (a) commits [first], (c) new list slots, (e) goals (every existing one
+    // [first], else those this batch created)
+    const int s0 = first ? L_imp : bc;
+    const int cn = first ? c_n : 0;
+    const int ns = Bc - s0;
+    const int tot1 = cn + ns + a.n_goals;
+    const int* cl = a.dirty + (size_t)c_buf * a.dcap;
+    for (int base = gwarp * 32; base < tot1; base += nwarps * 32) {        // warp-uniform
+        const int t = base + lane;
+        int v = -1;
+        if (t < cn) v = cl[t];
+        else if (t < cn + ns) v = bl[1 + s0 + (t - cn)];
+        else if (t < tot1) {
+            v = a.goals[t - cn - ns];
+            if (v >= n_all || (!first && v < n_old)) v = -1;
+        }
+        const bool want = v >= 0 && app_in_I(a, v) && atomicMax(&a.istamp[v], ks) < ks;
+        app_list_push(tl, tc, want, v);
+    }
+    // (b) [first] g-changed vertices and their out-neighbours, (d) [first]
+    // vertices appended by earlier appends since the last Improve: out-rows
+    if (first) {
+        const int* gl = a.gcl + (size_t)((k - 1) & 1) * a.dcap;
+        const int tot2 = gc_n + max(0, n_old - n_imp);
+        for (int i = gwarp; i < tot2; i += nwarps) {                      // warp-uniform
+            const int x = i < gc_n ? gl[i] : n_imp + (i - gc_n);
+            if (i < gc_n) {
+                const bool want = lane == 0 && app_in_I(a, x) && atomicMax(&a.istamp[x], ks) < ks;
+                app_list_push(tl, tc, want, x);
+            }
+            const long long o0 = a.oboff[x], o1 = a.oboff[x + 1];
+            const long long q0 = a.odoff_new[x], q1 = a.odoff_new[x + 1];
+            const long long L1 = o1 - o0, L = L1 + (q1 - q0);
+            for (long long kb = 0; kb < L; kb += 32) {
+                const long long e = kb + lane;
+                int w = -1;
+                if (e < L) w = e < L1 ? a.obidx[o0 + e] : a.odidx_new[q0 + (e - L1)];
+                const bool want = w >= 0 && app_in_I(a, w) && atomicMax(&a.istamp[w], ks) < ks;
+                app_list_push(tl, tc, want, w);
+            }
+        }
+    }
+    // (d) this batch: the heads of its edges whose tail is a new vertex
+    const long long m = a.m;
+    for (long long b0 = (long long)gwarp * 32; b0 < m; b0 += (long long)nwarps * 32) {   // warp-uniform
+        const long long e = b0 + lane;
+        int y0 = -1, y1 = -1;
+        if (e < m) {
+            const int sv = a.src[e], dv = a.dst[e];
+            if (sv >= n_old) y0 = dv;                         // sv -> dv
+            if (a.undirected && dv >= n_old) y1 = sv;         // dv -> sv
+        }
+        const bool w0 = y0 >= 0 && app_in_I(a, y0) && atomicMax(&a.istamp[y0], ks) < ks;
+        app_list_push(tl, tc, w0, y0);
+        const bool w1 = y1 >= 0 && app_in_I(a, y1) && atomicMax(&a.istamp[y1], ks) < ks;
+        app_list_push(tl, tc, w1, y1);
+    }
+    if (tid == 0) ctl->app_pre_k = k;
+}
+
 __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* cnt1,
                                                       long long* bsum) {
     cg::grid_group grid = cg::this_grid();
@@ -403,6 +550,19 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     if (threadIdx.x < 32) {
         const double t = warp_goal_cost(a.g, a.goals, a.n_goals, n_old);
         if (threadIdx.x == 0) s_thr = t;
+    }
+    // the next exploit's first Improve (P8): its counters are recomputed by
+    // every append, its task list continued while no Improve ran in between
+    const unsigned pre_k = *(volatile const unsigned*)&ctl->imp_count + 1u;
+    const bool pre_first = *(volatile const unsigned*)&ctl->app_pre_k != pre_k;
+    if (tid == 0) {
+        if (a.pre_ok) {
+            ctl->pre_relax[pre_k & 1] = 0;
+            ctl->pre_tasks[pre_k & 1] = 0;
+            if (pre_first) ctl->pre_count[pre_k & 1] = 0;
+        } else {
+            ctl->app_pre_k = 0;
+        }
     }
     // ---- P0 validation (R12)
     {
@@ -436,7 +596,10 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     }
     grid.sync();
     APP_MARK(0);
-    if (failed(ctl)) return;                              // uniform: err is final
+    if (failed(ctl)) {                                    // uniform: err is final
+        if (tid == 0) ctl->app_pre_k = 0;                 // (its counters were zeroed)
+        return;
+    }
     // ---- P1 old delta row lengths (both stores)
     //      and, for the copy in P4, the row holding the first entry of each
     //      kCopyChunk-entry chunk of the old deltas
@@ -751,6 +914,11 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         }
     }
     APP_MARK(8);
+    if (a.pre_ok) {
+        grid.sync();
+        append_prebuild(a, pre_k, pre_first, tid, nthreads, sm);
+        APP_MARK(11);
+    }
     if (tid == 0) ctl->app_ns[9] += 1;
 #undef APP_MARK
 }
