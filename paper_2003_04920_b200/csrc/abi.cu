@@ -354,6 +354,10 @@ int grow_hot_slab(pirrt_ctx* c, int64_t cap) {
             cp(dirty + dcap, c->dirty + c->dcap, 4 * std::min<int64_t>(n, c->dcap)) ||
             cp(gcl, c->gcl, 4 * std::min<int64_t>(n, c->dcap)) ||
             cp(gcl + dcap, c->gcl + c->dcap, 4 * std::min<int64_t>(n, c->dcap)) ||
+            // both task-list slots (an append's prebuilt list lives across
+            // appends; slot k & 1 starts at (k & 1) x capacity)
+            cp(alist, c->alist, 4 * std::min<int64_t>(n, c->g_cap)) ||
+            cp(alist + cap, c->alist + c->g_cap, 4 * std::min<int64_t>(n, c->g_cap)) ||
             cp(nbq[c->Bsel], c->Bq[c->Bsel], 4 * keep_cur))
             return fail(PIRRT_E_CUDA, "vertex slab copy failed");
         CU(cudaStreamSynchronize(s));
@@ -1885,6 +1889,27 @@ extern "C" int pirrt_debug_phases(const pirrt_ctx* c, unsigned long long* out, i
 extern "C" int pirrt_debug_append_phases(const pirrt_ctx* c, unsigned long long* out, int n) {
     if (!c || !out || n < 12) return fail(PIRRT_E_INVAL, "debug_append_phases: bad arguments");
     std::memcpy(out, c->ctl_host->app_ns, 12 * sizeof(unsigned long long));
+    return PIRRT_OK;
+}
+
+// debug: the incremental Improve's bookkeeping in DevCtl (synchronous read):
+// out[0..11] = imp_count, app_pre_k, pre_count[0], pre_count[1], c_buf, c_n,
+// L_imp, n_imp, gc_count[0], gc_count[1], imp_full, dirty_count[c_buf];
+// list (nullable): task list slot (imp_count + 1) & 1, up to cap entries
+extern "C" int pirrt_debug_inc(const pirrt_ctx* c, long long* out, int32_t* list, int64_t cap) {
+    if (!c || !out) return fail(PIRRT_E_INVAL, "debug_inc: bad arguments");
+    CU(cudaStreamSynchronize(c->stream));
+    DevCtl h;
+    CU(cudaMemcpy(&h, c->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost));
+    const long long v[12] = {h.imp_count, h.app_pre_k, h.pre_count[0], h.pre_count[1], h.c_buf, h.c_n,
+                             h.L_imp, h.n_imp, h.gc_count[0], h.gc_count[1], h.imp_full,
+                             h.dirty_count[h.c_buf & 1]};
+    std::memcpy(out, v, sizeof v);
+    if (list && cap > 0) {
+        const int slot = (int)((h.imp_count + 1) & 1);
+        const int64_t nl = std::min<int64_t>(cap, std::max(0, h.pre_count[slot]));
+        if (nl) CU(cudaMemcpy(list, c->alist + (size_t)slot * c->g_cap, nl * sizeof(int), cudaMemcpyDeviceToHost));
+    }
     return PIRRT_OK;
 }
 

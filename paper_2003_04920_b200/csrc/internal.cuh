@@ -159,6 +159,7 @@ struct DevCtl {
     // (0: none), slot app_pre_k & 1 of alist / pre_count / pre_relax / pre_tasks
     unsigned app_pre_k;
 };
+constexpr unsigned kPrePoison = 0x80000000u;   // app_pre_k | this: epoch without a prebuilt list
 
 // Everything the persistent exploit kernel touches.
 struct ExploitArgs {

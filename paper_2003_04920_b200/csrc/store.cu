@@ -389,9 +389,11 @@ __device__ __forceinline__ long long blk_excl_scan_ll(long long x, long long* sm
 // new edges) -- and the exploit's first Improve takes the list as prebuilt
 // (no discovery phase, no grid barrier).  The first append after an Improve
 // also lists (a), (b), (e) and whatever earlier appends added (exactly the
-// exploit's own discovery); later appends continue the list (stamps 2k:
-// below the 2k + 1 of a discovery of the same Improve, which runs whenever
-// the list is not valid).  The full Improve's counters over I (Sum of
+// exploit's own discovery); later appends continue the list.  Stamps per
+// Improve k: 4k an Evaluate's prebuilt list, 4k + 1 the append's, 4k + 2 a
+// discovery (which runs whenever no valid list exists), so each replaces
+// the ones below it.  Once an append of the epoch could not list its sources
+// (conditions, rejection), the epoch is poisoned: no later append continues.  The full Improve's counters over I (Sum of
 // in-degrees, |I|: the paper's relaxation count) are recomputed by every
 // append, since new in-edges change the members' in-degrees.  Valid under the
 // incremental Improve's own conditions (evaluated here on the same device
@@ -438,12 +440,12 @@ __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int
                     Bc - L_imp <= a.inc_max &&
                     (a.inc_imp > 1 || 4LL * (gc_n + (n_all - n_imp)) < (long long)live);
     if (!ok) {
-        if (tid == 0) ctl->app_pre_k = 0;
+        if (tid == 0) ctl->app_pre_k = k | kPrePoison;
         return;
     }
     int* tl = a.alist + (size_t)(k & 1u) * a.acap;
     int* tc = &ctl->pre_count[k & 1];
-    const unsigned ks = 2u * k;
+    const unsigned ks = 4u * k + 1u;       // above an Evaluate's list (4k), below a discovery (4k + 2)
     // the full Improve's counters over I (every member of the list, every
     // existing goal)
     long long rx = 0, tk = 0;
@@ -553,15 +555,20 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     }
     // the next exploit's first Improve (P8): its counters are recomputed by
     // every append, its task list continued while no Improve ran in between
+    // (app_pre_k: k = Improve k's list is valid; k | kPrePoison = an append
+    // since Improve k - 1 could not list its sources, so no later one may
+    // continue: the exploit discovers them itself)
     const unsigned pre_k = *(volatile const unsigned*)&ctl->imp_count + 1u;
-    const bool pre_first = *(volatile const unsigned*)&ctl->app_pre_k != pre_k;
+    const unsigned pre_st = *(volatile const unsigned*)&ctl->app_pre_k;
+    const bool pre_on = a.pre_ok && pre_st != (pre_k | kPrePoison);
+    const bool pre_first = pre_st != pre_k;
     if (tid == 0) {
-        if (a.pre_ok) {
+        if (pre_on) {
             ctl->pre_relax[pre_k & 1] = 0;
             ctl->pre_tasks[pre_k & 1] = 0;
             if (pre_first) ctl->pre_count[pre_k & 1] = 0;
         } else {
-            ctl->app_pre_k = 0;
+            ctl->app_pre_k = pre_k | kPrePoison;
         }
     }
     // ---- P0 validation (R12)
@@ -597,7 +604,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     grid.sync();
     APP_MARK(0);
     if (failed(ctl)) {                                    // uniform: err is final
-        if (tid == 0) ctl->app_pre_k = 0;                 // (its counters were zeroed)
+        if (tid == 0) ctl->app_pre_k = pre_k | kPrePoison;   // (its counters were zeroed)
         return;
     }
     // ---- P1 old delta row lengths (both stores)
@@ -914,7 +921,7 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
         }
     }
     APP_MARK(8);
-    if (a.pre_ok) {
+    if (pre_on) {
         grid.sync();
         append_prebuild(a, pre_k, pre_first, tid, nthreads, sm);
         APP_MARK(11);
