@@ -418,38 +418,53 @@ __device__ __forceinline__ void app_list_push(int* buf, int* cnt, bool want, int
     if (want) buf[base + __popc(m & lt)] = v;
 }
 
+// The current B list (the previous step's, for a deferred step) and its length.
+__device__ __forceinline__ const int* app_list(const AppendArgs& a, int* bc) {
+    if (a.dev_list) {                                     // written by the previous step's exploit
+        *bc = *(volatile const int*)&a.ctl->dev_Bcount;
+        return *(volatile const int*)&a.ctl->dev_Bsel ? a.Bq1 : a.Bq0;
+    }
+    *bc = a.Bcount;
+    return a.Blist;
+}
+
+// The incremental Improve's own conditions (exploit_kernel), decided before
+// the promising test with nprom <= n_new as the bound (an append that would
+// pass only with its exact count leaves the discovery to the exploit).
+__device__ __forceinline__ bool app_prebuild_ok(const AppendArgs& a, unsigned k, int bc) {
+    const DevCtl* ctl = a.ctl;
+    const int n_all = a.n_old + a.n_new;
+    const int imp_full = *(volatile const int*)&ctl->imp_full;
+    const int gc_n = *(volatile const int*)&ctl->gc_count[(k - 1) & 1];
+    const int c_n = *(volatile const int*)&ctl->c_n;
+    const int L_imp = *(volatile const int*)&ctl->L_imp, n_imp = *(volatile const int*)&ctl->n_imp;
+    const int live_min = bc - *(volatile const int*)&ctl->holes;
+    return !imp_full && gc_n < a.inc_max && c_n < a.inc_max && L_imp <= bc && n_imp <= n_all &&
+           (long long)bc + a.n_new - L_imp <= a.inc_max &&
+           (a.inc_imp > 1 || 4LL * (gc_n + (n_all - n_imp)) < (long long)live_min);
+}
+
+// Everything but this batch's new members (listed by the promising test
+// itself): runs in the promising test's phase, on state that phase does not
+// change (old list entries, old vertices' b, the row store after P5).
+// rx / tk carry the counters of the new members this thread listed.
 __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int tid, int nthreads,
-                                long long* sm) {
+                                long long rx, long long tk, long long* sm) {
     DevCtl* ctl = a.ctl;
     const int lane = threadIdx.x & 31;
     const int gwarp = tid >> 5, nwarps = nthreads >> 5;
     const int n_old = a.n_old, n_all = a.n_old + a.n_new;
-    const int* bl = a.Blist;
-    int bc = a.Bcount;
-    if (a.dev_list) {
-        bl = *(volatile const int*)&ctl->dev_Bsel ? a.Bq1 : a.Bq0;
-        bc = *(volatile const int*)&ctl->dev_Bcount;
-    }
-    const int Bc = bc + *(volatile const int*)&ctl->nprom;
-    const int imp_full = *(volatile const int*)&ctl->imp_full;
+    int bc;
+    const int* bl = app_list(a, &bc);
     const int gc_n = *(volatile const int*)&ctl->gc_count[(k - 1) & 1];
     const int c_n = *(volatile const int*)&ctl->c_n, c_buf = *(volatile const int*)&ctl->c_buf;
     const int L_imp = *(volatile const int*)&ctl->L_imp, n_imp = *(volatile const int*)&ctl->n_imp;
-    const int live = Bc - *(volatile const int*)&ctl->holes;
-    const bool ok = !imp_full && gc_n < a.inc_max && c_n < a.inc_max && L_imp <= Bc && n_imp <= n_all &&
-                    Bc - L_imp <= a.inc_max &&
-                    (a.inc_imp > 1 || 4LL * (gc_n + (n_all - n_imp)) < (long long)live);
-    if (!ok) {
-        if (tid == 0) ctl->app_pre_k = k | kPrePoison;
-        return;
-    }
     int* tl = a.alist + (size_t)(k & 1u) * a.acap;
     int* tc = &ctl->pre_count[k & 1];
     const unsigned ks = 4u * k + 1u;       // above an Evaluate's list (4k), below a discovery (4k + 2)
-    // the full Improve's counters over I (every member of the list, every
-    // existing goal)
-    long long rx = 0, tk = 0;
-    for (int t = tid; t < Bc; t += nthreads) {
+    // the full Improve's counters over I: the old list entries, every
+    // existing goal (+ the new members, counted when listed)
+    for (int t = tid; t < bc; t += nthreads) {
         const int v = bl[1 + t];
         if (v < 0 || is_goal(a.goals, a.n_goals, v)) continue;
         rx += app_in_degree(a, v);
@@ -467,18 +482,18 @@ __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int
         if (rx) atomicAdd((unsigned long long*)&ctl->pre_relax[k & 1], (unsigned long long)rx);
         if (tk) atomicAdd(&ctl->pre_tasks[k & 1], (int)tk);
     }
-    // (a) commits [first], (c) new list slots, (e) goals (every existing one
-    // [first], else those this batch created)
-    const int s0 = first ? L_imp : bc;
+    // (a) commits [first], (c) list slots of earlier appends since the last
+    // Improve [first], (e) goals (every existing one [first], else those this
+    // batch created)
     const int cn = first ? c_n : 0;
-    const int ns = Bc - s0;
+    const int ns = first ? bc - L_imp : 0;
     const int tot1 = cn + ns + a.n_goals;
     const int* cl = a.dirty + (size_t)c_buf * a.dcap;
     for (int base = gwarp * 32; base < tot1; base += nwarps * 32) {        // warp-uniform
         const int t = base + lane;
         int v = -1;
         if (t < cn) v = cl[t];
-        else if (t < cn + ns) v = bl[1 + s0 + (t - cn)];
+        else if (t < cn + ns) v = bl[1 + L_imp + (t - cn)];
         else if (t < tot1) {
             v = a.goals[t - cn - ns];
             if (v >= n_all || (!first && v < n_old)) v = -1;
@@ -504,27 +519,28 @@ __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int
                 const long long e = kb + lane;
                 int w = -1;
                 if (e < L) w = e < L1 ? a.obidx[o0 + e] : a.odidx_new[q0 + (e - L1)];
-                const bool want = w >= 0 && app_in_I(a, w) && atomicMax(&a.istamp[w], ks) < ks;
+                // (new heads are members -- listed by the promising test --
+                // or goals of this batch -- listed above -- or not in I)
+                const bool want = w >= 0 && w < n_old && app_in_I(a, w) && atomicMax(&a.istamp[w], ks) < ks;
                 app_list_push(tl, tc, want, w);
             }
         }
     }
-    // (d) this batch: the heads of its edges whose tail is a new vertex
+    // (d) this batch: the old heads of its edges whose tail is a new vertex
     const long long m = a.m;
     for (long long b0 = (long long)gwarp * 32; b0 < m; b0 += (long long)nwarps * 32) {   // warp-uniform
         const long long e = b0 + lane;
         int y0 = -1, y1 = -1;
         if (e < m) {
             const int sv = a.src[e], dv = a.dst[e];
-            if (sv >= n_old) y0 = dv;                         // sv -> dv
-            if (a.undirected && dv >= n_old) y1 = sv;         // dv -> sv
+            if (sv >= n_old && dv < n_old) y0 = dv;           // sv -> dv
+            if (a.undirected && dv >= n_old && sv < n_old) y1 = sv;   // dv -> sv
         }
         const bool w0 = y0 >= 0 && app_in_I(a, y0) && atomicMax(&a.istamp[y0], ks) < ks;
         app_list_push(tl, tc, w0, y0);
         const bool w1 = y1 >= 0 && app_in_I(a, y1) && atomicMax(&a.istamp[y1], ks) < ks;
         app_list_push(tl, tc, w1, y1);
     }
-    if (tid == 0) ctl->app_pre_k = k;
 }
 
 __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* cnt1,
@@ -888,6 +904,11 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
     // ---- P7 b(v) = g(v) + h(v) < g(x_goal); promising ones join the B list
     // (goal set, R4: the goal cost before the batch)
     const double thr = s_thr;
+    int bc_list;
+    int* const blist = const_cast<int*>(app_list(a, &bc_list));
+    const bool pre_go = pre_on && app_prebuild_ok(a, pre_k, bc_list);   // (uniform)
+    const unsigned pre_ks = 4u * pre_k + 1u;
+    long long pre_rx = 0, pre_tk = 0;
     for (int base = blockIdx.x * blockDim.x; base < n_new; base += nthreads) {
         const int i = base + threadIdx.x;
         const int v = n_old + i;
@@ -909,23 +930,18 @@ __global__ void __launch_bounds__(kBT) k_append_fused(AppendArgs a, long long* c
             pos = __shfl_sync(kFull, pos, leader);
             unsigned lt;
             asm("mov.u32 %0, %lanemask_lt;" : "=r"(lt));
-            if (p) {
-                int* bl = a.Blist;
-                int bc = a.Bcount;
-                if (a.dev_list) {                     // written by the previous step's exploit
-                    bl = *(volatile const int*)&ctl->dev_Bsel ? a.Bq1 : a.Bq0;
-                    bc = *(volatile const int*)&ctl->dev_Bcount;
-                }
-                bl[1 + bc + pos + __popc(mm & lt)] = v;
-            }
+            if (p) blist[1 + bc_list + pos + __popc(mm & lt)] = v;
+        }
+        if (pre_go) {
+            // (c) of the next exploit's first Improve: the new members
+            const bool want = p && atomicMax(&a.istamp[v], pre_ks) < pre_ks;
+            if (want && !is_goal(a.goals, a.n_goals, v)) { pre_rx += app_in_degree(a, v); ++pre_tk; }
+            app_list_push(a.alist + (size_t)(pre_k & 1u) * a.acap, &ctl->pre_count[pre_k & 1], want, v);
         }
     }
+    if (pre_go) append_prebuild(a, pre_k, pre_first, tid, nthreads, pre_rx, pre_tk, sm);
     APP_MARK(8);
-    if (pre_on) {
-        grid.sync();
-        append_prebuild(a, pre_k, pre_first, tid, nthreads, sm);
-        APP_MARK(11);
-    }
+    if (tid == 0 && pre_on) ctl->app_pre_k = pre_go ? pre_k : (pre_k | kPrePoison);
     if (tid == 0) ctl->app_ns[9] += 1;
 #undef APP_MARK
 }

@@ -264,3 +264,17 @@ def test_prebuilt_task_lists_and_small_grid(P, monkeypatch, env, d, n, S):
     gpu.exploit = rec
     dual_replay(gpu, orc, r, S, n_stop=min(n, 2 + 300 * S))
     assert sum(s.inc_improves for s in stats) > 0
+
+
+@pytest.mark.parametrize("d,n,S,gamma,pmax", [(6, 30000, 2048, "k", "1000000"), (2, 6000, 1, "star", "0"),
+                                              (3, 8000, 300, "k", "1000000"), (2, 6000, 7, "star", "1000000")])
+def test_append_prebuilt_first_improve(P, monkeypatch, d, n, S, gamma, pmax):
+    """The next exploit's first Improve listed by the append (P8) -- forced on
+    for large batches, off for S = 1 -- against the oracle: every counter
+    (relaxations = the full Improve's) and the state, bit for bit."""
+    monkeypatch.setenv("PIRRT_PREBUILD_MAX", pmax)
+    gm = gen.gamma_k(d) if gamma == "k" else gen.gamma_star(d)
+    r = gen.rrg(d, n, gm, n_boxes=12, seed=gen.seed_of("prebuild", d, S))
+    gpu = P.Context(h_root=r.h_root())
+    orc = Oracle(h_root=r.h_root())
+    dual_replay(gpu, orc, r, S, n_stop=min(n, 2 + 400 * S))
