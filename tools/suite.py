@@ -104,6 +104,8 @@ def exploit_summary(rows):
         "exploit_ms_mean": statistics.mean(ems) if ems else None,
         "iterations_mean": statistics.mean([r[2].iterations for r in ex]) if ex else None,
         "relaxations_total": sum(r[2].relaxations for r in ex),
+        "device_ms_median": pct([r[2].device_ms for r in ex], 50) if ex and hasattr(ex[0][2], "device_ms") else None,
+        "device_ms_p95": pct([r[2].device_ms for r in ex], 95) if ex and hasattr(ex[0][2], "device_ms") else None,
     }
 
 
@@ -173,7 +175,7 @@ def main():
     # cold solve (S = N): one append of everything, one exploit
     ctx, rows = gpu_replay(g6, n6, n6)
     st = rows[0][2]
-    bytes_ = st.relaxations * 20 + st.improve_set * 40 + st.eval_scanned * 8 + st.eval_visits * 38
+    bytes_ = bench.algo_bytes(st)                         # SURVEY.md 8(d) units over the work done
     rep["cfg3_6d_1M_gammak_cold_solve"] = {
         "append_ms": rows[0][0], "exploit_ms": rows[0][1], "device_ms": st.device_ms,
         "iterations": st.iterations, "evaluations": st.evaluations,
