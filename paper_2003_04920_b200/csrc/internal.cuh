@@ -233,6 +233,7 @@ struct ExploitArgs {
     int neighbours;                   // PIRRT_F_NEIGHBOURS (and not PRUNE_OFF): I = B u
                                       // N+(B u {root}) u G (R16, NEXT-4)
     int wide_tasks;                   // hand an Improve with |I| >= this to improve_wide_kernel (0: never)
+    int wide_lpv;                     // its lanes per vertex (16 or 32, by the mean degree)
     int it_base;                      // first PI iteration of this launch (1 = a fresh exploit)
     int resume;                       // 1: iteration it_base's Improve already ran (wide kernel)
     // children index for large Evaluates (build_children): |B| >= kids_min (0: never)
