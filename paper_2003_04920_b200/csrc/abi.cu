@@ -1039,7 +1039,11 @@ static int exploit_sharded(std::vector<pirrt_ctx*>& cs) {
         a.shard_dev = 1;
         a.shard_K = K;
         a.wide_tasks = c->wide_tasks;
-        if ((rc = grow(c->rec_local, c->rec_local_cap, rec_max + 1, 0, c->stream))) return rc;
+        // (sized by the vertex capacity, which grows geometrically, not by n:
+        // a reallocation inside the loop's first launch cost tens of ms)
+        if ((rc = grow(c->rec_local, c->rec_local_cap, std::max<int64_t>(rec_max, c->vcap / P + 2) + 1, 0,
+                       c->stream)))
+            return rc;
         if ((rc = grow(c->rec_all, c->rec_all_cap, (int64_t)P * (K + 1), 0, c->stream))) return rc;
         a.rec_count = &c->rec_local[0].v;
         a.rec_out = c->rec_local + 1;
@@ -1054,6 +1058,12 @@ static int exploit_sharded(std::vector<pirrt_ctx*>& cs) {
         CU(cudaStreamSynchronize(c->stream));           // (host sources above are on the stack)
     }
     int Bc_known = c0->Bcount, stop = 0, it = 1;
+    const bool dbg = std::getenv("PIRRT_DEBUG_HOST") != nullptr;
+    auto now_us = []() {
+        return std::chrono::duration<double, std::micro>(
+                   std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t_in = dbg ? now_us() : 0.0;
     auto evaluate_all = [&](int itv) -> int {
         for (size_t i = 0; i < G; ++i) {
             A[i].shard_K = K;
@@ -1076,6 +1086,7 @@ static int exploit_sharded(std::vector<pirrt_ctx*>& cs) {
             if ((rc = shard_exchange(cs, K))) return rc;
             if ((rc = evaluate_all(it))) return rc;
         }
+        const double t_enq = dbg ? now_us() : 0.0;
         stop = 0;
         for (size_t i = 0; i < G; ++i) {
             if ((rc = read_ctl(cs[i]))) return rc;
@@ -1085,6 +1096,8 @@ static int exploit_sharded(std::vector<pirrt_ctx*>& cs) {
             stop = si;
         }
         const DevCtl& h = *c0->ctl_host;
+        if (dbg) std::fprintf(stderr, "pirrt host: sharded chunk %d (it %d): enqueued +%.1f us, done +%.1f us, stop %d\n",
+                              chunk, it, t_enq - t_in, now_us() - t_in, h.shard_stop);
         Bc_known = h.Bcount_out;
         if (stop == 4) {                                  // a rank had more than K records
             const int it_o = h.shard_over_it;
