@@ -286,6 +286,7 @@ struct pirrt_ctx {
 
 constexpr int kStepDepth = 2;
 constexpr int kStepHead = 1020;
+constexpr size_t kStepHeadBytes = sizeof(int) * (4 + kStepHead);
 
 namespace {
 
@@ -449,8 +450,7 @@ void free_all(pirrt_ctx* c) {
     if (c->rdone) cudaFree(c->rdone);
     if (c->fold_mark) cudaFree(c->fold_mark);
     for (auto& sl : c->slot) {
-        if (sl.ctl) cudaFreeHost(sl.ctl);
-        if (sl.head) cudaFreeHost(sl.head);
+        if (sl.ctl) cudaFreeHost(sl.ctl);                 // (head lives inside it)
         if (sl.dpath) cudaFree(sl.dpath);
         for (cudaEvent_t e : {sl.e0, sl.e1, sl.done})
             if (e) cudaEventDestroy(e);
@@ -739,7 +739,9 @@ int pirrt_create(const pirrt_config* cfg_in, pirrt_ctx** out) {
     if (cudaMemcpyAsync(c->goals, goal_ids.data(), goal_ids.size() * sizeof(int),
                         cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
         return bail(fail(PIRRT_E_CUDA, "create: goals copy"));
-    if (cudaMalloc(&c->ctl, sizeof(DevCtl)) != cudaSuccess) return bail(fail(PIRRT_E_NOMEM, "ctl"));
+    // the control block, followed by a deferred step's best-path head (one
+    // read-back per step)
+    if (cudaMalloc(&c->ctl, sizeof(DevCtl) + kStepHeadBytes) != cudaSuccess) return bail(fail(PIRRT_E_NOMEM, "ctl"));
     if (cudaMallocHost(&c->ctl_host, sizeof(DevCtl)) != cudaSuccess)
         return bail(fail(PIRRT_E_NOMEM, "ctl host"));
     if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
@@ -867,9 +869,8 @@ int pirrt_graph_append_batch(pirrt_ctx* c, int32_t n_new, const double* h_new,
     if ((rc = grow(c->odidx[nb], c->odidx_cap[nb], dneed, 0, s))) return rc;
     if (early) CU(cudaStreamWaitEvent(s, c->copy_done, 0));
     else if ((rc = stage_all(s))) return rc;
-    CU(cudaMemsetAsync(&c->ctl->err, 0, 2 * sizeof(int), s));   // err, sweeps
-    CU(cudaMemsetAsync(&c->ctl->nprom, 0, sizeof(int), s));
-    CU(cudaMemsetAsync(&c->ctl->sweep_changed[0], 0, 2 * sizeof(int), s));
+    static_assert(offsetof(DevCtl, nprom) == offsetof(DevCtl, err) + 2 * sizeof(int), "DevCtl layout");
+    CU(cudaMemsetAsync(&c->ctl->err, 0, 3 * sizeof(int), s));   // err, sweeps, nprom
     if ((rc = grow(c->app_chunk, c->app_chunk_cap, 2 * (c->delta_edges / kAppendCopyChunk + 2), 0, s)))
         return rc;
     AppendArgs a;
@@ -1283,11 +1284,11 @@ int complete_pending(pirrt_ctx* c) {
 // then the new exploit is not started and the failure is reported now.
 int step_slot_init(pirrt_ctx* c, pirrt_ctx::StepSlot& sl) {
     if (!sl.ctl) {
-        if (cudaMallocHost(&sl.ctl, sizeof(DevCtl)) != cudaSuccess ||
-            cudaMallocHost(&sl.head, sizeof(int) * (4 + kStepHead)) != cudaSuccess) {
+        if (cudaMallocHost(&sl.ctl, sizeof(DevCtl) + kStepHeadBytes) != cudaSuccess) {
             cudaGetLastError();
             return fail(PIRRT_E_NOMEM, "step_async: pinned slot");
         }
+        sl.head = (int*)(sl.ctl + 1);                     // the best-path head after the block
         CU(cudaEventCreate(&sl.e0));
         CU(cudaEventCreate(&sl.e1));
         CU(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
@@ -1451,9 +1452,8 @@ int pirrt_step_async(pirrt_ctx* c, int32_t n_new, const double* h_new, int64_t n
         CU(cudaStreamWaitEvent(s, c->copy_done, 0));
     }
     // append (Extend's local relaxation and promising test, R14 / P:184-188)
-    CU(cudaMemsetAsync(&c->ctl->err, 0, 2 * sizeof(int), s));   // err, sweeps
-    CU(cudaMemsetAsync(&c->ctl->nprom, 0, sizeof(int), s));
-    CU(cudaMemsetAsync(&c->ctl->sweep_changed[0], 0, 2 * sizeof(int), s));
+    static_assert(offsetof(DevCtl, nprom) == offsetof(DevCtl, err) + 2 * sizeof(int), "DevCtl layout");
+    CU(cudaMemsetAsync(&c->ctl->err, 0, 3 * sizeof(int), s));   // err, sweeps, nprom
     if ((rc = grow(c->app_chunk, c->app_chunk_cap, 2 * (c->delta_edges / kAppendCopyChunk + 2), 0, s)))
         return rc;
     AppendArgs a;
@@ -1495,11 +1495,12 @@ int pirrt_step_async(pirrt_ctx* c, int32_t n_new, const double* h_new, int64_t n
     CU(cudaEventRecord(sl.e1, s));
     sl.blocks = blocks;
     // path read-out (Alg. 1 lines 8-12) into the slot
-    CU(launch_best_path(c->parent, c->g, c->n, c->goals, (int)c->goals_host.size(), sl.dpath, s));
+    CU(launch_best_path(c->parent, c->g, c->n, c->goals, (int)c->goals_host.size(), sl.dpath, s,
+                        (int*)(c->ctl + 1), kStepHead));
     c->launches += g_kernel_launches - l0;
-    CU(cudaMemcpyAsync(sl.head, sl.dpath, sizeof(int) * (4 + kStepHead), cudaMemcpyDeviceToHost, s));
+    // one read-back: the control block's tail and the best-path head after it
     const size_t o = offsetof(DevCtl, status);
-    CU(cudaMemcpyAsync((char*)sl.ctl + o, (const char*)c->ctl + o, sizeof(DevCtl) - o,
+    CU(cudaMemcpyAsync((char*)sl.ctl + o, (const char*)c->ctl + o, sizeof(DevCtl) - o + kStepHeadBytes,
                        cudaMemcpyDeviceToHost, s));
     CU(cudaEventRecord(sl.done, s));
     ++c->steps_out;

@@ -112,16 +112,16 @@ struct DevCtl {
     int handoff, handoff_it;
     unsigned long long t_wide0, t_wide1;   // ~min start / max end of the wide Improve
     // append / set_policy (the words every block may update on their own lines)
+    // (err, sweeps, nprom: one memset before each append)
     alignas(128) int err;         // bitmask of kErr*
-    int sweeps;                   // local-relaxation sweeps
+    int sweeps;                   // local-relaxation passes (1: the dataflow pass)
+    int nprom;                    // new promising vertices (one atomic per warp that has some)
     // append phase timeline (lead thread, %globaltimer ns, accumulated over
     // appends; pirrt_debug_append_phases): 0 validation, 1 old row lengths,
     // 2 histogram, 3 scan partials, 4 row offsets, 5 old-delta copy, 6
     // scatter + init, 7 local relaxation, 8 promising test, 9 appends;
     // 10 block 0's own time in the P4 chunk copy, 11 the prebuild (P8)
-    unsigned long long app_ns[12];
-    alignas(128) int nprom;       // new promising vertices
-    alignas(128) int sweep_changed[2];
+    alignas(128) unsigned long long app_ns[12];
     // ---- persistent across exploits (zeroed only at create): the state
     // the incremental Evaluate needs ("incremental
     // Evaluate").  Written by the lead thread after an Evaluate's last grid
@@ -418,7 +418,7 @@ cudaError_t launch_extend_grid(const ExtendArgs& a, cudaStream_t s);   // grid, 
 cudaError_t launch_extend_edges(const ExtendArgs& a, cudaStream_t s);  // the triples
 
 cudaError_t launch_best_path(const int* parent, const double* g, int n, const int* goals,
-                             int n_goals, int* out, cudaStream_t s);
+                             int n_goals, int* out, cudaStream_t s, int* head = nullptr, int head_n = 0);
 
 // device-wide exclusive scan: out[0..L] with out[L] = total
 cudaError_t scan_exclusive(const long long* in, long long* out, long long L,

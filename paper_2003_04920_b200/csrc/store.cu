@@ -304,8 +304,10 @@ __global__ void k_jump_any(const int* anc, int n, DevCtl* ctl) {
 // its branch (Alg. 1 lines 8-12).
 // out[0] = length (-1: cycle), out[1] = best goal (-1: none reached),
 // out[2..3] = its g bits, out[4..] = goal..root
+// head (nullable): the header and the first head_n entries again (a
+// deferred step reads them back together with the control block)
 __global__ void k_best_path(const int* parent, const double* g, int n, const int* goals,
-                            int n_goals, int* out) {
+                            int n_goals, int* out, int* head, int head_n) {
     int best = -1;
     double gb = INFINITY;
     for (int i = 0; i < n_goals; ++i) {                 // ascending ids: strict < keeps the lowest
@@ -317,10 +319,16 @@ __global__ void k_best_path(const int* parent, const double* g, int n, const int
     *(double*)&out[2] = gb;
     int v = best, len = 0;
     while (v != -1 && len <= n) {
+        if (head && len < head_n) head[4 + len] = v;
         out[4 + len++] = v;
         v = parent[v];
     }
     out[0] = (v == -1) ? len : -1;
+    if (head) {
+        head[0] = out[0];
+        head[1] = best;
+        *(double*)&head[2] = gb;
+    }
 }
 
 
@@ -1067,9 +1075,9 @@ cudaError_t launch_rebuild_blist(const unsigned char* b, int n, int* list, int* 
 }
 
 cudaError_t launch_best_path(const int* parent, const double* g, int n, const int* goals,
-                             int n_goals, int* out, cudaStream_t s) {
+                             int n_goals, int* out, cudaStream_t s, int* head, int head_n) {
     ++g_kernel_launches;
-    k_best_path<<<1, 1, 0, s>>>(parent, g, n, goals, n_goals, out);
+    k_best_path<<<1, 1, 0, s>>>(parent, g, n, goals, n_goals, out, head, head_n);
     return cudaGetLastError();
 }
 
