@@ -45,7 +45,7 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     from paper_2003_04920_b200 import pirrt
     lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "pirrt.h"', 'int main(void) {']
-    for st in (pirrt.pirrt_config, pirrt.pirrt_exploit_stats):
+    for st in (pirrt.pirrt_config, pirrt.pirrt_exploit_stats, pirrt.pirrt_step_result):
         lines.append(f'printf("{st.__name__} size %zu\\n", sizeof({st.__name__}));')
         for f, _ in st._fields_:
             lines.append(f'printf("{st.__name__} {f} %zu\\n", offsetof({st.__name__}, {f}));')
@@ -56,7 +56,7 @@ def test_struct_layouts_match_header(tmp_path):
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
     out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
     got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
-    for st in (pirrt.pirrt_config, pirrt.pirrt_exploit_stats):
+    for st in (pirrt.pirrt_config, pirrt.pirrt_exploit_stats, pirrt.pirrt_step_result):
         assert got[(st.__name__, "size")] == C.sizeof(st)
         for f, _ in st._fields_:
             assert got[(st.__name__, f)] == getattr(st, f).offset, (st.__name__, f)
