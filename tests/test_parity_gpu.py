@@ -327,13 +327,15 @@ def test_level_to_work_queue_handover_6d(P, monkeypatch, gb):
     dual_replay(gpu, orc, r, 700)
 
 
+@pytest.mark.parametrize("lpv", ["16", "32"])
 @pytest.mark.parametrize("wide", ["1", "300"])
 @pytest.mark.parametrize("flags", [0, PRUNE_OFF])
-def test_wide_improve_handoff_parity(P, monkeypatch, wide, flags):
+def test_wide_improve_handoff_parity(P, monkeypatch, wide, flags, lpv):
     # every Improve with |I| >= PIRRT_WIDE_TASKS runs as the full-occupancy
-    # launch (hand-off and resume of the persistent loop): same bits, same
-    # counters as the oracle
+    # launch (hand-off and resume of the persistent loop), with 16 or 32
+    # lanes per vertex: same bits, same counters as the oracle
     monkeypatch.setenv("PIRRT_WIDE_TASKS", wide)
+    monkeypatch.setenv("PIRRT_WIDE_LPV", lpv)
     r = gen.rrg(6, 12000, gen.gamma_k(6), n_boxes=10, seed=gen.seed_of("wide", wide, flags))
     gpu = P.Context(h_root=r.h_root(), flags=flags)
     orc = Oracle(h_root=r.h_root(), flags=flags)
