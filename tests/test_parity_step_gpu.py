@@ -181,3 +181,21 @@ def test_step_errors(P):
     with pytest.raises(P.PirrtError) as e:      # unusable afterwards
         gpu.best_path()
     assert e.value.code == P.PIRRT_E_STATE
+
+
+@pytest.mark.parametrize("variant", ["prune_off", "neighbours", "eps"])
+def test_step_variants(P, variant):
+    """Deferred steps under the configuration variants (classical PI, the
+    NEIGHBOURS Improve set, epsilon > 0) against the oracle's synchronous step."""
+    from paper_2003_04920_b200.berrt import batches
+    r = gen.rrg(3, 6000, gen.gamma_k(3), n_boxes=8, seed=gen.seed_of("step-var", variant))
+    kw, okw = {}, {}
+    if variant == "prune_off":
+        kw["flags"], okw["flags"] = P.PIRRT_F_PRUNE_OFF, oracle.PRUNE_OFF
+    elif variant == "neighbours":
+        kw["flags"], okw["flags"] = P.PIRRT_F_NEIGHBOURS, oracle.NEIGHBOURS
+    else:
+        kw["epsilon"] = okw["epsilon"] = 1e-3
+    gpu = P.Context(h_root=r.h_root(), **kw)
+    orc = Oracle(h_root=r.h_root(), **okw)
+    run_pipelined(P, gpu, orc, r, list(batches(r.n, 211)), where=variant)
