@@ -805,7 +805,23 @@ def main_sharded(a, rank, world):
     total_ms, cold_ms, e2e_ms = pdist.max_over_ranks([sum(step_ms), cold.device_ms,
                                                       e0.elapsed_time(e1)])
     relax, relax_cold = pdist.sum_over_ranks([sum(s.relaxations for s in ex), cold.relaxations])
+    # the exploits alone (device time, slowest rank) and their 8(d) bytes
+    # summed over the ranks (each rank's counters cover its share)
+    ex_ms_tot, = pdist.max_over_ranks([sum(s.device_ms for s in ex)])
+    byt, pbyt = pdist.sum_over_ranks([sum(algo_bytes(s) for s in ex), sum(paper_bytes(s) for s in ex)])
+    peak, peak_src = peaks()
     if rank == 0:
+        ach = byt / (ex_ms_tot * 1e-3) / 1e9 if ex_ms_tot > 0 else 0.0
+        pach = pbyt / (ex_ms_tot * 1e-3) / 1e9 if ex_ms_tot > 0 else 0.0
+        roofline = {"kernel": "sharded exploit (shard_improve_kernel + record all-gather + "
+                              "shard_evaluate_kernel per PI iteration)",
+                    "bound": "hbm", "achieved": round(ach, 2), "peak": peak, "peak_source": peak_src,
+                    "unit": "GB/s", "frac": round(ach / peak / max(1, world), 5),
+                    "frac_note": "of the peak of all the job's GPUs",
+                    "algorithmic_bytes_per_launch": round(byt / max(1, len(ex))),
+                    "formula": ALGO_FORMULA,
+                    "paper_units": {"achieved": round(pach, 2), "frac": round(pach / peak / max(1, world), 5)},
+                    "traffic": None, "traffic_source": None}
         ms_step = total_ms / K
         line = {
             "metric": METRIC, "value": round(ms_step, 4), "unit": "ms", "n_gpus": world,
@@ -818,6 +834,10 @@ def main_sharded(a, rank, world):
                        "step": "extend(S points, device) + exploit-to-convergence (sharded)",
                        "parallelism": f"sharded{world}" if world > 1 else "single"},
             "gteps": round(relax / (total_ms * 1e-3) / 1e9, 4),
+            "exploit_ms_stats": stats_summary([s.device_ms for s in ex]),
+            "exploit_ms_mean": round(ex_ms_tot / max(1, len(ex)), 4),
+            "exploit_gteps": round(relax / (ex_ms_tot * 1e-3) / 1e9, 4) if ex_ms_tot else 0,
+            "roofline": roofline,
             "cold_solve": {"exploit_ms": round(cold_ms, 4), "iterations": cold.iterations,
                            "gteps": round(relax_cold / (cold_ms * 1e-3) / 1e9, 3)},
             "build_s": round(t_build, 2), "clocks": clk, "cpu_baseline": None,
