@@ -229,7 +229,10 @@ int pirrt_exploit_wait(pirrt_ctx* ctx, pirrt_exploit_stats* stats);
  * its result in *out (nullable) and its best path root..goal in
  * path_out[0..out->path_len) (nullable; E_RANGE if cap is smaller, the rest
  * of *out is still filled).  Results are identical to the synchronous calls.
- * While a step is outstanding every other call returns E_STATE.
+ * While a step is outstanding every other call on the context returns
+ * E_STATE, except pirrt_step_wait, pirrt_steps_outstanding, the counters
+ * (pirrt_num_vertices / num_edges / kernel_launches: the vertices and edges
+ * of every enqueued step are counted) and pirrt_destroy (which waits).
  * Errors of step_async: E_INVAL as the append's argument checks, and
  * PIRRT_F_VALIDATE (use the synchronous append); E_STATE two steps already
  * outstanding, a sharded context, or a context with a world.  A batch the
@@ -250,7 +253,7 @@ int pirrt_step_async(pirrt_ctx* ctx, int32_t n_new, const double* h_new, int64_t
                      const pirrt_vid* src, const pirrt_vid* dst, const double* cost,
                      uint32_t flags);
 int pirrt_step_wait(pirrt_ctx* ctx, pirrt_step_result* out, pirrt_vid* path_out, int64_t cap);
-int pirrt_steps_outstanding(const pirrt_ctx* ctx);
+int pirrt_steps_outstanding(const pirrt_ctx* ctx);   /* steps enqueued and not yet waited */
 
 /* Read-out of the vertex state the paper's GPU version keeps per vertex
  * (the cost-to-come g, the parent pointer of the policy
