@@ -969,6 +969,7 @@ static void fill_exploit_args(pirrt_ctx* c, ExploitArgs& a, int blocks) {
     // wide Improve: a warp per vertex for long rows (measured: gamma* mean
     // degree 1,138 +14% with 32 lanes; gamma_k ~60-80 +30% slower with 32)
     a.wide_lpv = c->wide_lpv > 0 ? c->wide_lpv : (mean_deg >= 192.0 ? 32 : 16);
+    a.num_sms = c->num_sms;
 }
 
 // Sharded exploit: per PI iteration

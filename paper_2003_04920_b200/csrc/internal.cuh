@@ -234,6 +234,8 @@ struct ExploitArgs {
                                       // N+(B u {root}) u G (R16, NEXT-4)
     int wide_tasks;                   // hand an Improve with |I| >= this to improve_wide_kernel (0: never)
     int wide_lpv;                     // its lanes per vertex (16 or 32, by the mean degree)
+    int num_sms;                      // the device's SMs (a grid of at most one block per SM
+                                      // runs the one-block-per-SM instantiation)
     int it_base;                      // first PI iteration of this launch (1 = a fresh exploit)
     int resume;                       // 1: iteration it_base's Improve already ran (wide kernel)
     // children index for large Evaluates (build_children): |B| >= kids_min (0: never)
