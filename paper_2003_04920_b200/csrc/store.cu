@@ -410,6 +410,12 @@ __device__ __forceinline__ bool app_in_I(const AppendArgs& a, int v) {
     return v != kRoot && (a.b[v] || is_goal(a.goals, a.n_goals, v));
 }
 
+// membership and the list stamp in one round trip (see exploit.cu list_candidate)
+__device__ __forceinline__ bool app_candidate(const AppendArgs& a, int v, unsigned ks) {
+    const bool fresh = atomicMax(&a.istamp[v], ks) < ks;
+    return app_in_I(a, v) && fresh;
+}
+
 __device__ __forceinline__ long long app_in_degree(const AppendArgs& a, int v) {
     return (a.boff[v + 1] - a.boff[v]) + (a.doff_new[v + 1] - a.doff_new[v]);
 }
@@ -506,7 +512,7 @@ __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int
             v = a.goals[t - cn - ns];
             if (v >= n_all || (!first && v < n_old)) v = -1;
         }
-        const bool want = v >= 0 && app_in_I(a, v) && atomicMax(&a.istamp[v], ks) < ks;
+        const bool want = v >= 0 && app_candidate(a, v, ks);
         app_list_push(tl, tc, want, v);
     }
     // (b) [first] g-changed vertices and their out-neighbours, (d) [first]
@@ -517,7 +523,7 @@ __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int
         for (int i = gwarp; i < tot2; i += nwarps) {                      // warp-uniform
             const int x = i < gc_n ? gl[i] : n_imp + (i - gc_n);
             if (i < gc_n) {
-                const bool want = lane == 0 && app_in_I(a, x) && atomicMax(&a.istamp[x], ks) < ks;
+                const bool want = lane == 0 && app_candidate(a, x, ks);
                 app_list_push(tl, tc, want, x);
             }
             const long long o0 = a.oboff[x], o1 = a.oboff[x + 1];
@@ -529,7 +535,7 @@ __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int
                 if (e < L) w = e < L1 ? a.obidx[o0 + e] : a.odidx_new[q0 + (e - L1)];
                 // (new heads are members -- listed by the promising test --
                 // or goals of this batch -- listed above -- or not in I)
-                const bool want = w >= 0 && w < n_old && app_in_I(a, w) && atomicMax(&a.istamp[w], ks) < ks;
+                const bool want = w >= 0 && w < n_old && app_candidate(a, w, ks);
                 app_list_push(tl, tc, want, w);
             }
         }
@@ -544,9 +550,9 @@ __device__ void append_prebuild(const AppendArgs& a, unsigned k, bool first, int
             if (sv >= n_old && dv < n_old) y0 = dv;           // sv -> dv
             if (a.undirected && dv >= n_old && sv < n_old) y1 = sv;   // dv -> sv
         }
-        const bool w0 = y0 >= 0 && app_in_I(a, y0) && atomicMax(&a.istamp[y0], ks) < ks;
+        const bool w0 = y0 >= 0 && app_candidate(a, y0, ks);
         app_list_push(tl, tc, w0, y0);
-        const bool w1 = y1 >= 0 && app_in_I(a, y1) && atomicMax(&a.istamp[y1], ks) < ks;
+        const bool w1 = y1 >= 0 && app_candidate(a, y1, ks);
         app_list_push(tl, tc, w1, y1);
     }
 }
