@@ -62,3 +62,128 @@ def test_bench_workload_full_size_parity():
     gp, gc, gg = gpu.best_path_goal()
     op, oc, og = orc.best_path_goal()
     assert np.array_equal(gp, op) and gc == oc and gg == og
+
+
+@pytest.mark.parametrize("k0", [0, 180])
+def test_gamma_star_7d_full_size_handoff_parity(k0):
+    """configs[3] at its full size and the headline radius: 7-D, 200k
+    vertices, gamma* (mean degree ~1,250, ~2.3e8 directed edges, 30 boxes),
+    built on the GPU by the device Extend in BE-RRT# batches of 1000 with the
+    Alg. 3 guard.  At batch k0 (180 = 20 batches before the end; 0 = from
+    the empty graph, so the one Replan on this workload that changes the
+    policy -- batch 0: 3 PI iterations, 2 Evaluates; the gamma* radius in
+    7-D is ~0.8 at n = 1000 and the best path never improves after it, see
+    tools/gstar7_probe.py -- is compared too), the stored graph
+    (pirrt_get_in_edges) and the policy state are handed to the oracle
+    (append + set_policy); then every remaining batch runs on both -- the
+    oracle is fed the edges the device Extend stored for that batch -- and
+    every Replan is compared bitwise: g, parent, pc, b, every counter, the
+    best path at the end."""
+    from paper_2003_04920_b200 import pirrt
+    from paper_2003_04920_b200.berrt import batches
+    d, n, S, boxes = 7, 200_000, 1000, 30
+    gm = gen.gamma_star(d)
+    pts, bx = gen.points(d, n, boxes, seed=gen.seed_of("fullsize-gstar", d, n))
+    h_root = float(np.sqrt(((pts[0] - pts[1]) ** 2).sum()))
+    # h as the device Extend computes it: squared differences summed in
+    # coordinate order, IEEE sqrt
+    s2 = np.zeros(n)
+    for k in range(d):
+        u = pts[:, k] - pts[1, k]
+        s2 = s2 + u * u
+    h = np.sqrt(s2)
+    gpu = pirrt.Context(h_root=h_root, vertex_capacity=n + 1024, edge_capacity=int(2.2 * 700 * n))
+    gpu.set_world(d, bx, pts[0], pts[1], gm)
+    bl = list(batches(n, S))
+    for lo, hi in bl[:k0]:
+        if gpu.extend(pts[lo:hi])[0] > 0:
+            gpu.exploit()
+    # hand-off
+    n0 = gpu.n
+    parent, g, _, b = gpu.state()
+    off, src, cost = gpu.in_edges()
+    assert off[-1] == gpu.n_edges
+    dst = np.repeat(np.arange(n0, dtype=np.int32), np.diff(off))
+    orc = Oracle(h_root=h_root)
+    if n0 > 2:
+        orc.append(h[2:n0], src, dst, cost)
+        orc.set_policy(parent, g, b)
+    del src, dst, cost, off
+    assert_same_state(gpu, orc, "after hand-off")
+    # the remaining batches: the device Extend, then the oracle fed the
+    # edges it stored (those touching the batch's new vertices)
+    replans = evals = 0
+    for k, (lo, hi) in enumerate(bl[k0:k0 + 20]):
+        n_old = gpu.n
+        pg = gpu.extend(pts[lo:hi])[0]
+        n_new = gpu.n
+        off, src, cost = gpu.in_edges()
+        dst = np.repeat(np.arange(n_new, dtype=np.int32), np.diff(off))
+        sel = (src >= n_old) | (dst >= n_old)
+        po = orc.append(h[n_old:n_new], src[sel], dst[sel], cost[sel])
+        del src, dst, cost, off, sel
+        assert pg == po, f"batch {k0 + k}: promising {pg} vs {po}"
+        if po > 0:
+            st = orc.exploit()
+            assert_same_stats(gpu.exploit(), st, f"batch {k0 + k}")
+            replans += 1
+            evals += st.evaluations
+        assert_same_state(gpu, orc, f"batch {k0 + k}")
+    gp, gc, gg = gpu.best_path_goal()
+    op, oc, og = orc.best_path_goal()
+    assert np.array_equal(gp, op) and gc == oc and gg == og
+    print(f"gamma* 7-D: hand-off at n={n0}, {n_old} -> {n_new} vertices, {gpu.n_edges} directed edges, "
+          f"{replans} Replans, {evals} Evaluates compared, path cost {gc:.6f}")
+    assert replans > 0 and (k0 == 180) == (n_new == n)
+
+
+def test_gamma_star_1m_cold_solve_full_size_parity():
+    """The bench line's gamma* cold solve at its full size (bench.py
+    gamma_star_record, same seed): configs[2]'s 6-D 1M samples, 20 boxes,
+    radius gamma* (~1.1e9 directed edges), every vertex added by the device
+    Extend with no Replan in between, then one Replan from that state.  The
+    stored graph and the Extend-relaxed state are handed to the oracle, both
+    run the cold Replan, and g, parent, pc, b, every counter and the best path
+    are compared bitwise.  Host memory ~45 GB, a few minutes."""
+    import time
+    import torch
+    from paper_2003_04920_b200 import pirrt
+    d, n, boxes, seed = 6, 1_000_000, 20, 0
+    gm = gen.gamma_star(d)
+    pts, bx = gen.points(d, n, boxes, seed=gen.seed_of("cfg3_gstar", d, n, boxes, seed))
+    h_root = float(np.sqrt(((pts[0] - pts[1]) ** 2).sum()))
+    gpu = pirrt.Context(h_root=h_root, vertex_capacity=n + 1024, edge_capacity=int(2.2 * 600 * n))
+    gpu.set_world(d, bx, pts[0], pts[1], gm)
+    dpts = torch.from_numpy(pts).cuda()
+    for lo in range(2, n, 131072):
+        gpu.extend(dpts[lo:min(n, lo + 131072)])
+    del dpts
+    s2 = np.zeros(n)
+    for k in range(d):
+        u = pts[:, k] - pts[1, k]
+        s2 = s2 + u * u
+    h = np.sqrt(s2)
+    t0 = time.perf_counter()
+    parent, g, _, b = gpu.state()
+    off, src, cost = gpu.in_edges()
+    m = int(off[-1])
+    assert m == gpu.n_edges and m > 1e9
+    dst = np.repeat(np.arange(n, dtype=np.int32), np.diff(off))
+    del off
+    orc = Oracle(h_root=h_root)
+    orc.append(h[2:], src, dst, cost)
+    del src, dst, cost
+    orc.set_policy(parent, g, b)
+    assert_same_state(gpu, orc, "after hand-off")
+    t1 = time.perf_counter()
+    st = orc.exploit()
+    t2 = time.perf_counter()
+    sg = gpu.exploit()
+    assert_same_stats(sg, st, "cold solve")
+    assert_same_state(gpu, orc, "cold solve")
+    gp, gc, gg = gpu.best_path_goal()
+    op, oc, og = orc.best_path_goal()
+    assert np.array_equal(gp, op) and gc == oc and gg == og
+    print(f"gamma* 6-D 1M cold solve: {m} directed edges, iterations={st.iterations} "
+          f"evaluations={st.evaluations} relaxations={st.relaxations}; GPU {sg.device_ms:.2f} ms, "
+          f"oracle {t2 - t1:.1f} s (hand-off {t1 - t0:.1f} s); path cost {gc:.6f}")
