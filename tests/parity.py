@@ -111,6 +111,15 @@ class RankGroup:
         assert len(set(got)) == 1, got
         return got[0]
 
+    def set_world(self, *args):
+        for c in self.ranks:
+            c.set_world(*args)
+
+    def extend(self, *args, **kw):
+        got = [c.extend(*args, **kw) for c in self.ranks]
+        assert len(set(got)) == 1, got
+        return got[0]
+
     def exploit(self):
         import dataclasses
         sts = self.P.group_exploit(self.ranks)

@@ -16,14 +16,18 @@ import pytest
 
 import gen
 from oracle import EDGES_UNDIRECTED, Oracle
-from parity import assert_same_state, assert_same_stats
+from parity import RankGroup, assert_same_state, assert_same_stats
 
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bench_workload_full_size_parity():
+@pytest.mark.parametrize("nranks", [1, 2])
+def test_bench_workload_full_size_parity(nranks):
+    """nranks = 2: the same at P = 2 -- an in-process group (the sharded
+    kernels, owner-partitioned in-edge store, record all-gather as device
+    copies; tests/test_parity_group_gpu.py) on one GPU."""
     import torch
     sys.path.insert(0, ROOT)
     import bench
@@ -35,8 +39,9 @@ def test_bench_workload_full_size_parity():
     S = a.S
     n0 = a.n - 4 * S
     stream = torch.cuda.current_stream()
-    gpu = pirrt.Context(h_root=g.h_root(), stream=stream, vertex_capacity=g.n + 1024,
-                        edge_capacity=int(2.4 * g.off[-1]) + 4096)
+    kw = dict(h_root=g.h_root(), stream=stream, vertex_capacity=g.n + 1024,
+              edge_capacity=int(2.4 * g.off[-1]) + 4096)
+    gpu = pirrt.Context(**kw) if nranks == 1 else RankGroup(pirrt, nranks, **kw)
     for lo, hi in batches(n0, S):
         s, d_, c = g.batch(lo, hi, directed=False)
         if gpu.append(g.h[lo:hi], s, d_, c, flags=EDGES_UNDIRECTED) > 0:
@@ -187,3 +192,74 @@ def test_gamma_star_1m_cold_solve_full_size_parity():
     print(f"gamma* 6-D 1M cold solve: {m} directed edges, iterations={st.iterations} "
           f"evaluations={st.evaluations} relaxations={st.relaxations}; GPU {sg.device_ms:.2f} ms, "
           f"oracle {t2 - t1:.1f} s (hand-off {t1 - t0:.1f} s); path cost {gc:.6f}")
+
+
+def test_cfg4_10m_sharded_cold_solve_full_size_parity():
+    """configs[4] at its full size: the 10M-vertex 6-D gamma_k RRG (20 boxes)
+    built by the device Extend in S = 65536 batches, as bench.py's sharded
+    leg builds it, then its cold solve (bench.py main_sharded's `cold`
+    sub-record) three ways: the oracle (state and stored graph handed over
+    from a one-rank context), that context, and the sharded kernels as
+    an in-process group of P = 2 on this GPU (vertex v's Improve on rank v mod 2,
+    record all-gather as device copies).  g, parent, pc, b, every counter and
+    the best path compared bitwise; the group's per-rank relaxation shares
+    sum to the oracle's count."""
+    import time
+    import torch
+    from paper_2003_04920_b200 import pirrt
+    d, n, S, boxes = 6, 10_000_000, 65536, 20
+    gm = gen.gamma_k(d)
+    pts, bx = gen.points(d, n, boxes, seed=gen.seed_of("fullsize-cfg4", d, n, boxes))
+    h_root = float(np.sqrt(((pts[0] - pts[1]) ** 2).sum()))
+    dpts = torch.from_numpy(pts).cuda()
+
+    def build(c):
+        c.set_world(d, bx, pts[0], pts[1], gm)
+        for lo in range(2, n, S):
+            c.extend(dpts[lo:min(n, lo + S)])
+        return c
+
+    one = build(pirrt.Context(h_root=h_root, vertex_capacity=n + 1024, edge_capacity=int(2.2 * 45 * n)))
+    s2 = np.zeros(n)
+    for k in range(d):
+        u = pts[:, k] - pts[1, k]
+        s2 = s2 + u * u
+    h = np.sqrt(s2)
+    t0 = time.perf_counter()
+    parent, g, _, b = one.state()
+    off, src, cost = one.in_edges()
+    m = int(off[-1])
+    assert m == one.n_edges
+    dst = np.repeat(np.arange(n, dtype=np.int32), np.diff(off))
+    del off
+    orc = Oracle(h_root=h_root)
+    orc.append(h[2:], src, dst, cost)
+    del src, dst, cost
+    orc.set_policy(parent, g, b)
+    assert_same_state(one, orc, "after hand-off")
+    t1 = time.perf_counter()
+    st = orc.exploit()
+    t2 = time.perf_counter()
+    op, oc, og = orc.best_path_goal()
+
+    def check(c, name):
+        assert_same_stats(c.exploit(), st, f"cold solve, {name}")
+        assert_same_state(c, orc, f"cold solve, {name}")
+        cp, cc, cg = c.best_path_goal()
+        assert np.array_equal(cp, op) and cc == oc and cg == og
+
+    check(one, "one rank")
+    one.close()
+    del one
+    # the group: P stores on this GPU, each sized for the graph just built (P
+    # = 4 does not fit one GPU's memory at this size; tests/
+    # test_parity_group_gpu.py covers P = 3, 4 at smaller sizes)
+    for P in (2,):
+        grp = build(RankGroup(pirrt, P, h_root=h_root, vertex_capacity=n + 1024, edge_capacity=int(1.3 * m)))
+        check(grp, f"P = {P}")
+        for c in grp.ranks:
+            c.close()
+        del grp
+    print(f"configs[4] 10M cold solve: {m} directed edges, iterations={st.iterations} "
+          f"evaluations={st.evaluations} relaxations={st.relaxations}; oracle {t2 - t1:.1f} s "
+          f"(hand-off {t1 - t0:.1f} s)")
