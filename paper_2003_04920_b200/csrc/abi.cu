@@ -268,6 +268,9 @@ struct pirrt_ctx {
     int* x_src = nullptr; int64_t x_src_cap = 0;
     int* x_dst = nullptr; int64_t x_dst_cap = 0;
     double* x_cost = nullptr; int64_t x_cost_cap = 0;
+    int* x_hj = nullptr; int64_t x_hj_cap = 0;           // the count pass's hit cache
+    double* x_hd = nullptr; int64_t x_hd_cap = 0;
+    int x_hcap = 128;             // hit-cache slots per new vertex (from the last batch's mean)
     bool in_extend = false;       // the append is pirrt_extend_batch's own
     // deferred BE-RRT# steps (pirrt_step_async / pirrt_step_wait): a ring of
     // kStepDepth slots, each the step's read-back (control block tail, best
@@ -442,7 +445,8 @@ void free_all(pirrt_ctx* c) {
                     c->s_src, c->s_dst, c->s_cost, c->s_h, c->s_parent, c->s_g, c->s_pc, c->s_b,
                     c->rec_local, c->rec_all, c->app_bsum, c->goals,
                     c->w_boxes, c->w_goal, c->pts, c->x_cell, c->x_cpts, c->x_ccnt, c->x_cstart,
-                    c->x_tmp, c->x_R, c->x_h, c->x_ecnt, c->x_eoff, c->x_src, c->x_dst, c->x_cost};
+                    c->x_tmp, c->x_R, c->x_h, c->x_ecnt, c->x_eoff, c->x_src, c->x_dst, c->x_cost,
+                    c->x_hj, c->x_hd};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
@@ -1860,7 +1864,19 @@ int pirrt_extend_batch(pirrt_ctx* c, int32_t n_new, const double* points, uint32
         if ((rc = grow(c->x_cstart, c->x_cstart_cap, ncell + 1, 0, s))) return rc;
     }
     CU(cudaMemcpyAsync(c->x_R, R.data(), sizeof(double) * n_new, cudaMemcpyHostToDevice, s));
+    // hit cache: the count pass keeps up to hcap (neighbour, distance) pairs
+    // per new vertex, so the write pass copies them instead of searching
+    // again (only vertices with more hits are searched twice); bounded to
+    // 1 GiB, off when the expected degree is beyond the cap
+    int hcap = c->x_hcap;
+    if ((int64_t)n_new * hcap * 12 > (1ll << 30)) hcap = (int)((1ll << 30) / (12ll * n_new));
+    if (hcap < 16) hcap = 0;
+    if (hcap > 0) {
+        if ((rc = grow(c->x_hj, c->x_hj_cap, (int64_t)n_new * hcap, 0, s))) return rc;
+        if ((rc = grow(c->x_hd, c->x_hd_cap, (int64_t)n_new * hcap, 0, s))) return rc;
+    }
     ExtendArgs a;
+    a.hcap = hcap; a.hj = c->x_hj; a.hd = c->x_hd;
     a.pts = c->pts; a.n_old = n_old; a.n_new = n_new; a.d = d; a.m = mc; a.brute = brute;
     a.ncell = ncell; a.cell = c->x_cell; a.ccnt = c->x_ccnt; a.cstart = c->x_cstart; a.cpts = c->x_cpts;
     a.scan_tmp = c->x_tmp; a.R = c->x_R; a.boxes = c->w_boxes; a.n_boxes = c->w_nboxes;
@@ -1877,6 +1893,12 @@ int pirrt_extend_batch(pirrt_ctx* c, int32_t n_new, const double* points, uint32
     a.src = c->x_src; a.dst = c->x_dst; a.cost = c->x_cost;
     if (total > 0) CU(launch_extend_edges(a, s));
     c->launches += g_kernel_launches - l0;
+    {   // next batch's cache: twice this batch's mean hits, a power of two in [32, 512], else off
+        const double mean = (double)total / n_new;
+        int hc = 32;
+        while (hc < 2.0 * mean && hc < 1024) hc *= 2;
+        c->x_hcap = hc > 512 ? 0 : hc;
+    }
     if (n_edges_out) *n_edges_out = total;
     // the ordinary append (a1): store, Extend's local relaxation, promising test
     c->in_extend = true;

@@ -103,7 +103,8 @@ __global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_ne
                              int brute, const long long* __restrict__ cstart,
                              const int* __restrict__ cpts, const double* __restrict__ R,
                              const double* __restrict__ boxes, int n_boxes, long long* cnt,
-                             const long long* __restrict__ off, int* src, int* dst, double* cost) {
+                             const long long* __restrict__ off, int* src, int* dst, double* cost,
+                             int hcap, int* __restrict__ hj, double* __restrict__ hd) {
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -117,6 +118,15 @@ __global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_ne
         const double inv_m = 1.0 / m;
         long long found = 0;
         const long long base = WRITE ? off[t] : 0;
+        if (WRITE && hcap > 0 && off[t + 1] - base <= hcap) {
+            // every hit is in the count pass's cache, in output order
+            const int nh = (int)(off[t + 1] - base);
+            const long long h0 = (long long)t * hcap;
+            for (int k = lane; k < nh; k += 32) {
+                src[base + k] = hj[h0 + k]; dst[base + k] = i; cost[base + k] = hd[h0 + k];
+            }
+            continue;
+        }
         int lo[16], rad[16];
         int N = 1;
         if (!brute) {
@@ -202,6 +212,10 @@ __global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_ne
                     const long long o = base + found + __popc(mask & lt);
                     src[o] = j; dst[o] = i; cost[o] = dd;
                 }
+                if (!WRITE && hit && hcap > 0) {
+                    const long long o = found + __popc(mask & lt);
+                    if (o < hcap) { hj[(long long)t * hcap + o] = j; hd[(long long)t * hcap + o] = dd; }
+                }
                 found += __popc(mask);
             }
             if (brute) break;
@@ -232,7 +246,7 @@ cudaError_t launch_extend_grid(const ExtendArgs& a, cudaStream_t s) {
     ++g_kernel_launches;
     k_neighbours<false><<<xgrid((long long)a.n_new * 32), kXT, 0, s>>>(
         a.pts, a.n_old, a.n_new, a.d, a.m, a.brute, a.cstart, a.cpts, a.R, a.boxes, a.n_boxes,
-        a.ecnt, nullptr, nullptr, nullptr, nullptr);
+        a.ecnt, nullptr, nullptr, nullptr, nullptr, a.hcap, a.hj, a.hd);
     if ((e = scan_exclusive(a.ecnt, a.eoff, a.n_new, a.scan_tmp, s)) != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -241,7 +255,7 @@ cudaError_t launch_extend_edges(const ExtendArgs& a, cudaStream_t s) {
     ++g_kernel_launches;
     k_neighbours<true><<<xgrid((long long)a.n_new * 32), kXT, 0, s>>>(
         a.pts, a.n_old, a.n_new, a.d, a.m, a.brute, a.cstart, a.cpts, a.R, a.boxes, a.n_boxes,
-        nullptr, a.eoff, a.src, a.dst, a.cost);
+        nullptr, a.eoff, a.src, a.dst, a.cost, a.hcap, a.hj, a.hd);
     return cudaGetLastError();
 }
 

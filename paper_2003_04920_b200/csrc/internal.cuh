@@ -415,6 +415,8 @@ struct ExtendArgs {
     long long* ecnt;              // [n_new + 1] edges per new vertex
     long long* eoff;              // [n_new + 1] their offsets (eoff[n_new] = total)
     int* src; int* dst; double* cost;   // [total] COO out (undirected: j -> i stored once)
+    int hcap;                     // hit-cache slots per new vertex (0: none)
+    int* hj; double* hd;          // [n_new][hcap] the count pass's hits, in output order
 };
 cudaError_t launch_extend_grid(const ExtendArgs& a, cudaStream_t s);   // grid, h, counts, offsets
 cudaError_t launch_extend_edges(const ExtendArgs& a, cudaStream_t s);  // the triples
