@@ -99,7 +99,10 @@ __device__ __forceinline__ bool seg_hits_box(const double* q, const double* p, c
 // tested 32 at a time (owner cell of a candidate by a binary search over the
 // lanes' prefix), so every lane works whatever the cell occupancy.
 template <bool WRITE>
-__global__ void k_neighbours(const double* __restrict__ pts, int n_old, int n_new, int d, int m,
+// 4 blocks per SM (64 registers, no spill): the count pass is bound by the
+// latency of its candidate gathers, so resident warps matter (ncu: 68
+// registers and 3 blocks before; profiles/r2/extend_count_ncu.json)
+__global__ void __launch_bounds__(kXT, 4) k_neighbours(const double* __restrict__ pts, int n_old, int n_new, int d, int m,
                              int brute, const long long* __restrict__ cstart,
                              const int* __restrict__ cpts, const double* __restrict__ R,
                              const double* __restrict__ boxes, int n_boxes, long long* cnt,
